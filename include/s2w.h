@@ -1,0 +1,126 @@
+/*
+ * s2w.h -- C ABI of the B200-native spherical-wavelet hot path.
+ *
+ * Drop-in boundary for the reference package `sphwav` (arXiv 1211.1680,
+ * /root/reference/pkg/src/sphwav).  The reference exposes this path only as
+ * Python functions; every entry point below replaces one of them and keeps its
+ * argument meaning, layout and error behaviour:
+ *
+ *   s2w_grid_nodes            <- grid.py:112-131   (_cached_grid / make_grid)
+ *   s2w_assoc_legendre_ring   <- sht.py:190-206    (assoc_legendre_ring)
+ *   s2w_sh_synthesis          <- sht.py:222-290    (sh_synthesis_stack / sh_synthesis)
+ *   s2w_sh_analysis           <- sht.py:293-355    (sh_analysis_stack / sh_analysis;
+ *                                                   additionally supports MW grids)
+ *   s2w_wav_analysis_harmonic <- transform.py:129-150 (wav_analysis_harmonic)
+ *   s2w_wav_synthesis_harmonic<- transform.py:153-172 (wav_synthesis_harmonic)
+ *   s2w_wav_analysis_pixel    <- transform.py:175-191 (wav_analysis_pixel)
+ *   s2w_wav_synthesis_pixel   <- transform.py:194-202 (wav_synthesis_pixel)
+ *
+ * Conventions ("contiguous 64-bit float buffers plus scalar
+ * parameters; no object graphs cross the boundary"):
+ *   - harmonic coefficients: complex128 interleaved (re, im) doubles, flat index
+ *     l*l + l + m (sht.py:50-52), L*L entries per set; sets are contiguous;
+ *   - maps: theta-major rows (grid.py:143), n_theta = L rings of n_phi = 2L-1
+ *     samples; complex maps are interleaved (re, im) doubles, real maps
+ *     (is_real = 1) are plain doubles (the imaginary part is exactly zero by
+ *     construction, grid.py:160);
+ *   - all data pointers are DEVICE pointers (CUDA global memory) except where a
+ *     parameter says "host"; `stream` is a cudaStream_t (NULL = legacy default);
+ *   - every call is asynchronous on `stream` and returns a status code; a plan is
+ *     used by one host thread at a time; distinct plans are independent.
+ *
+ * Status codes map onto the reference's exception hierarchy (errors.py:4-13):
+ *   S2W_EPARAM -> ParameterError, everything else -> SphwavError/RuntimeError.
+ */
+#ifndef S2W_H
+#define S2W_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S2W_OK 0
+#define S2W_EPARAM 1    /* domain violation: ParameterError (errors.py:8)       */
+#define S2W_ECUDA 2     /* CUDA runtime failure                                 */
+#define S2W_ENOMEM 3    /* device allocation failure                            */
+#define S2W_EINTERNAL 4 /* invariant broken inside the library                  */
+
+#define S2W_SCHEME_GL 0 /* SamplingScheme.GL (grid.py:33-35)                   */
+#define S2W_SCHEME_MW 1 /* SamplingScheme.MW                                   */
+
+typedef struct s2w_sht_plan s2w_sht_plan;
+typedef struct s2w_wav_plan s2w_wav_plan;
+
+/* Library version string ("s2w-b200 x.y.z"). */
+const char* s2w_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* s2w_last_error(void);
+
+/* Host-only: ring colatitudes theta[L] and, for GL, the Gauss-Legendre weights
+ * over cos(theta) (weights may be NULL; for MW they are not defined and the
+ * array is left untouched).  grid.py:93-124.  No GPU needed. */
+int s2w_grid_nodes(int scheme, int L, double* theta, double* weights);
+
+/* table[l*L + m] = orthonormal P_lm(cos theta) for 0 <= m <= l < L, zero above
+ * the diagonal (sht.py:190-206, without the reference's 1e-280 flush).
+ * `table` is a device buffer of L*L doubles. */
+int s2w_assoc_legendre_ring(int L, double theta, double* table, void* stream);
+
+/* ---------------------------------------------------------------- SHT */
+/* Plan for spherical harmonic transforms on one grid (scheme, L) of `device`. */
+int s2w_sht_plan_create(int scheme, int L, int device, s2w_sht_plan** plan);
+int s2w_sht_plan_destroy(s2w_sht_plan* plan);
+
+/* map[s] = synthesis of flm[s] (band L_coef <= plan L, zero-padded above it)
+ * for s < n_sets.  is_real: coefficient sets carry the real-signal symmetry;
+ * the output map is then real (n_sets*L*(2L-1) doubles).  MW: the south-pole
+ * ring is pinned to its m = 0 value (sht.py:274-279). */
+int s2w_sh_synthesis(s2w_sht_plan* plan, int n_sets, int L_coef, int is_real,
+                     const double* flm, double* map, void* stream);
+
+/* flm[s] (n_sets*L*L complex) = exact analysis of map[s].  GL: Gauss-Legendre
+ * quadrature (sht.py:308-346).  MW: McEwen-Wiaux sampling theorem (theta
+ * extension + |sin| convolution), which the reference lacks (sht.py:300-303).
+ * is_real: map is real; negative orders are written as (-1)^m conj(f_lm)
+ * exactly (sht.py:328-331). */
+int s2w_sh_analysis(s2w_sht_plan* plan, int n_sets, int is_real, const double* map,
+                    double* flm, void* stream);
+
+/* ---------------------------------------------------------------- wavelets */
+/* Plan for the axisymmetric wavelet transform of `batch` maps at band L.
+ *   n_kern   = 1 + number of wavelet scales (scaling kernel first, then j0..J)
+ *   kernels  = HOST array [n_kern][L]: Phi_l0 then Psi^j_l0 (tiling.py:219-245)
+ *   bands    = HOST array [n_kern]: band limit of each coefficient map
+ *              (multires: scaling_bandlimit, scale_bandlimits; full-res: all L;
+ *               transform.py:108-114)
+ * The plan precomputes sqrt(4 pi/(2l+1)) * K_j(l) (transform.py:117-126). */
+int s2w_wav_plan_create(int scheme, int L, int batch, int is_real, int n_kern,
+                        const double* kernels, const int* bands, int device,
+                        s2w_wav_plan** plan);
+int s2w_wav_plan_destroy(s2w_wav_plan* plan);
+
+/* Harmonic tiling.  outs[j] receives batch sets of band_j^2 coefficients
+ * (truncate != 0) or L^2 coefficients (truncate == 0). */
+int s2w_wav_analysis_harmonic(s2w_wav_plan* plan, int truncate, const double* flm,
+                              double* const* outs, void* stream);
+/* flm (batch*L*L) = sum_j sqrt(4pi/(2l+1)) K_j(l) pad(ins[j]); ins[j] has
+ * band_j^2 (or L^2 when full_band != 0) coefficients per set. */
+int s2w_wav_synthesis_harmonic(s2w_wav_plan* plan, int full_band, const double* const* ins,
+                               double* flm, void* stream);
+
+/* map (batch maps at L) -> scale_maps[j] (batch maps at band_j), j < n_kern. */
+int s2w_wav_analysis_pixel(s2w_wav_plan* plan, const double* map, double* const* scale_maps,
+                           void* stream);
+/* scale_maps[j] -> map (exact inverse of s2w_wav_analysis_pixel). */
+int s2w_wav_synthesis_pixel(s2w_wav_plan* plan, const double* const* scale_maps, double* map,
+                            void* stream);
+
+/* Coefficient workspace of the plan (batch*L*L complex, device): after
+ * s2w_wav_analysis_pixel it holds f_lm of the input map; after
+ * s2w_wav_synthesis_pixel the recombined f_lm (transform.py:196-200). */
+int s2w_wav_plan_flm(s2w_wav_plan* plan, double** flm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S2W_H */

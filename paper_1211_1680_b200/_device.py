@@ -1,0 +1,131 @@
+"""Device plumbing: torch CUDA tensors, streams and cached C-ABI plans.
+
+PyTorch provides device memory, pinned staging buffers and the current CUDA
+stream; all arithmetic on the hot path happens in libs2w.so kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native
+from .errors import SphwavError
+
+_lock = threading.Lock()
+_sht_plans: dict = {}
+_wav_plans: dict = {}
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda() -> None:
+    t = torch()
+    if not t.cuda.is_available():
+        raise SphwavError(
+            "s2w requires a CUDA device (B200, sm_100a); there is no CPU fallback"
+        )
+    _native.load()
+
+
+def device_index() -> int:
+    return torch().cuda.current_device()
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(tensor.data_ptr())
+
+
+def to_device(arr: np.ndarray):
+    """Host numpy -> CUDA tensor through a pinned staging buffer."""
+    t = torch()
+    host = t.from_numpy(np.require(arr, requirements=["C", "W"]))
+    if host.numel() * host.element_size() >= (1 << 20):
+        host = host.pin_memory()
+    return host.to(device=f"cuda:{device_index()}", non_blocking=True)
+
+
+def to_host(tensor) -> np.ndarray:
+    return tensor.cpu().numpy()
+
+
+def empty(n: int, dtype="float64"):
+    t = torch()
+    return t.empty(n, dtype=getattr(t, dtype), device=f"cuda:{device_index()}")
+
+
+class ShtPlan:
+    """Owner of an ``s2w_sht_plan`` (one grid on one device)."""
+
+    def __init__(self, scheme_code: int, L: int, device: int):
+        lib = _native.load()
+        h = ctypes.c_void_p()
+        _native.check(lib.s2w_sht_plan_create(scheme_code, L, device, ctypes.byref(h)))
+        self.handle, self.L, self.device = h, L, device
+
+    def __del__(self):
+        try:
+            _native.load().s2w_sht_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def sht_plan(scheme_code: int, L: int) -> ShtPlan:
+    key = (scheme_code, L, device_index())
+    with _lock:
+        p = _sht_plans.get(key)
+        if p is None:
+            p = ShtPlan(scheme_code, L, key[2])
+            _sht_plans[key] = p
+        return p
+
+
+class WavPlan:
+    """Owner of an ``s2w_wav_plan``: tiling factors, per-scale grids, workspaces."""
+
+    def __init__(self, scheme_code, L, batch, real, kernels: np.ndarray, bands, device):
+        lib = _native.load()
+        kern = np.ascontiguousarray(kernels, dtype=np.float64)
+        nk = kern.shape[0]
+        bands_c = (ctypes.c_int * nk)(*[int(b) for b in bands])
+        h = ctypes.c_void_p()
+        _native.check(
+            lib.s2w_wav_plan_create(
+                scheme_code, L, batch, int(bool(real)), nk,
+                kern.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), bands_c, device,
+                ctypes.byref(h),
+            )
+        )
+        self.handle, self.L, self.batch, self.real = h, L, batch, bool(real)
+        self.n_kern, self.bands, self.device = nk, tuple(int(b) for b in bands), device
+
+    def __del__(self):
+        try:
+            _native.load().s2w_wav_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def wav_plan(scheme_code, L, batch, real, kernels, bands) -> WavPlan:
+    kern = np.ascontiguousarray(kernels, dtype=np.float64)
+    key = (scheme_code, L, batch, bool(real), kern.tobytes(), tuple(bands), device_index())
+    with _lock:
+        p = _wav_plans.get(key)
+        if p is None:
+            p = WavPlan(scheme_code, L, batch, real, kern, bands, key[-1])
+            _wav_plans[key] = p
+        return p
+
+
+def ptr_array(tensors):
+    arr = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    return arr

@@ -1,0 +1,84 @@
+"""ctypes binding of the sm_100a C-ABI library ``lib/libs2w.so`` (include/s2w.h).
+
+There is no CPU fallback: importing works without a GPU (host-only entry
+points such as ``s2w_grid_nodes`` are usable), but every compute entry point
+requires the CUDA library and a CUDA device, and fails loudly otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import ParameterError, SphwavError
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libs2w.so"
+
+S2W_OK, S2W_EPARAM = 0, 1
+SCHEME_GL, SCHEME_MW = 0, 1
+
+_c_int, _c_double, _vp = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+
+_PROTOS = {
+    "s2w_version": (ctypes.c_char_p, []),
+    "s2w_last_error": (ctypes.c_char_p, []),
+    "s2w_grid_nodes": (_c_int, [_c_int, _c_int, _dp, _dp]),
+    "s2w_assoc_legendre_ring": (_c_int, [_c_int, _c_double, _vp, _vp]),
+    "s2w_sht_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
+    "s2w_sht_plan_destroy": (_c_int, [_vp]),
+    "s2w_sh_synthesis": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "s2w_sh_analysis": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _vp]),
+    "s2w_wav_plan_create": (
+        _c_int,
+        [_c_int, _c_int, _c_int, _c_int, _c_int, _dp, ctypes.POINTER(_c_int), _c_int,
+         ctypes.POINTER(_vp)],
+    ),
+    "s2w_wav_plan_destroy": (_c_int, [_vp]),
+    "s2w_wav_plan_flm": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "s2w_wav_analysis_harmonic": (_c_int, [_vp, _c_int, _vp, ctypes.POINTER(_vp), _vp]),
+    "s2w_wav_synthesis_harmonic": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_wav_analysis_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
+    "s2w_wav_synthesis_pixel": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+}
+
+EXPORTED_SYMBOLS = tuple(_PROTOS)
+
+_lib = None
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load libs2w.so (once).  Raises RuntimeError if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise RuntimeError(
+            f"s2w CUDA library not found at {_LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (or `make`)"
+        )
+    lib = ctypes.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
+    for name, (res, args) in _PROTOS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    """Translate a C-ABI status into the reference's exception types."""
+    if status == S2W_OK:
+        return
+    msg = load().s2w_last_error().decode(errors="replace")
+    if status == S2W_EPARAM:
+        raise ParameterError(msg)
+    raise SphwavError(f"s2w status {status}: {msg}")
+
+
+def version() -> str:
+    return load().s2w_version().decode()

@@ -1,0 +1,978 @@
+// C ABI (include/s2w.h): plans, precomputed tables and the host-side
+// orchestration of the hot path.  Host code only; kernels live in
+// fft_kernels.cu, legendre_kernels.cu and tiling_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "s2w.h"
+#include "s2w_internal.h"
+
+using namespace s2w;
+
+#define S2W_VERSION "s2w-b200 0.1.0"
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? S2W_ENOMEM : S2W_ECUDA, "%s: %s (%s:%d)", \
+                  #x, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define CHECK(x)            \
+  do {                      \
+    int r_ = (x);           \
+    if (r_ != S2W_OK) return r_; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Plain device allocation owned by a plan (freed in the plan destructor).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  int ensure(size_t n) {
+    if (n <= bytes && p) return S2W_OK;
+    release();
+    if (n == 0) n = 16;
+    CU(cudaMalloc(&p, n));
+    bytes = n;
+    return S2W_OK;
+  }
+  template <class T>
+  int upload(const std::vector<T>& v) {
+    CHECK(ensure(v.size() * sizeof(T)));
+    if (!v.empty()) CU(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return S2W_OK;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+// ------------------------------------------------------------------ grids (host)
+typedef long double ld;
+static const ld PI_L = 3.141592653589793238462643383279502884L;
+
+// Legendre P_n(x) and P_n'(x) in extended precision.
+static void legendre_pd(int n, ld x, ld& p, ld& dp) {
+  ld p0 = 1.0L, p1 = x;
+  if (n == 0) {
+    p = 1.0L;
+    dp = 0.0L;
+    return;
+  }
+  for (int k = 2; k <= n; ++k) {
+    ld p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+    p0 = p1;
+    p1 = p2;
+  }
+  p = p1;
+  dp = n * (x * p1 - p0) / (x * x - 1.0L);
+}
+
+// Gauss-Legendre nodes ordered north -> south (x descending) with weights,
+// Newton iteration in 80-bit precision (grid.py:93-124 semantics).
+static void gl_nodes(int L, std::vector<double>& theta, std::vector<double>& w) {
+  theta.resize(L);
+  w.resize(L);
+  if (L == 1) {
+    theta[0] = std::acos(0.0);
+    w[0] = 2.0;
+    return;
+  }
+  for (int i = 0; i < L; ++i) {
+    ld x = std::cos(PI_L * (i + 0.75L) / (L + 0.5L));
+    ld p, dp;
+    for (int it = 0; it < 100; ++it) {
+      legendre_pd(L, x, p, dp);
+      ld dx = p / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-19L) break;
+    }
+    legendre_pd(L, x, p, dp);
+    x -= p / dp;
+    legendre_pd(L, x, p, dp);
+    ld wi = 2.0L / ((1.0L - x * x) * dp * dp);
+    theta[i] = std::acos((double)x);
+    w[i] = (double)wi;
+  }
+}
+
+static void mw_nodes(int L, std::vector<double>& theta) {
+  theta.resize(L);
+  for (int t = 0; t < L; ++t) theta[t] = (double)(2 * t + 1) * M_PI / (double)(2 * L - 1);
+}
+
+// ------------------------------------------------------------------ host FFT (tables)
+typedef std::complex<ld> cld;
+
+static int ilog2_ceil(long long n) {
+  int l = 0;
+  while ((1LL << l) < n) ++l;
+  return l;
+}
+
+static unsigned bitrev(unsigned p, int bits) {
+  unsigned r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((p >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+// In-place forward DFT (exp(-2 pi i jk/M)), M a power of two, extended precision.
+static void fft_ld(std::vector<cld>& a) {
+  const size_t n = a.size();
+  const int bits = ilog2_ceil((long long)n);
+  for (size_t i = 0; i < n; ++i) {
+    size_t j = bitrev((unsigned)i, bits);
+    if (j > i) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const size_t h = len / 2;
+    std::vector<cld> w(h);
+    for (size_t j = 0; j < h; ++j) {
+      ld ang = -2.0L * PI_L * (ld)j / (ld)len;
+      w[j] = cld(std::cos(ang), std::sin(ang));
+    }
+    for (size_t i = 0; i < n; i += len)
+      for (size_t j = 0; j < h; ++j) {
+        cld u = a[i + j], v = a[i + j + h] * w[j];
+        a[i + j] = u + v;
+        a[i + j + h] = u - v;
+      }
+  }
+}
+
+static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
+
+// spectrum (natural order) / M, stored at bit-reversed positions
+static std::vector<double2> spectrum_brev(std::vector<cld> a) {
+  const size_t M = a.size();
+  const int bits = ilog2_ceil((long long)M);
+  fft_ld(a);
+  std::vector<double2> out(M);
+  for (size_t p = 0; p < M; ++p) out[p] = d2(a[bitrev((unsigned)p, bits)] / (ld)M);
+  return out;
+}
+
+// ------------------------------------------------------------------ per-device seed table
+static const int SEED_KMAX = 16384;
+
+struct DeviceTables {
+  double* seed_c = nullptr;  // c_m, m < SEED_KMAX
+};
+
+static std::mutex g_mu;
+static std::map<int, DeviceTables> g_dev;
+
+static int device_tables(int dev, DeviceTables** out) {
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) {
+    *out = &it->second;
+    return S2W_OK;
+  }
+  std::vector<double> c(SEED_KMAX);
+  ld v = 1.0L / std::sqrt(4.0L * PI_L);
+  c[0] = (double)v;
+  for (int m = 1; m < SEED_KMAX; ++m) {
+    v *= std::sqrt((ld)(2 * m + 1) / (ld)(2 * m));
+    c[m] = (double)v;
+  }
+  DeviceTables t;
+  CU(cudaMalloc(&t.seed_c, sizeof(double) * SEED_KMAX));
+  CU(cudaMemcpy(t.seed_c, c.data(), sizeof(double) * SEED_KMAX, cudaMemcpyHostToDevice));
+  g_dev[dev] = t;
+  *out = &g_dev[dev];
+  return S2W_OK;
+}
+
+// ------------------------------------------------------------------ grid resources
+struct GridRes {
+  int device, scheme, k, N, logM;
+  std::vector<int2> act_host;
+  double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
+  int2* act = nullptr;
+  double2 *tw = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
+          *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
+  double* seed_c = nullptr;
+
+  FftTablesDev fft() const {
+    FftTablesDev t;
+    t.N = N;
+    t.logM = logM;
+    t.tw = tw;
+    t.chirp = chirp;
+    t.bl_fwd = bl_fwd;
+    t.bl_inv = bl_inv;
+    t.ph1 = ph1;
+    t.ph2 = ph2;
+    t.wconv = wconv;
+    return t;
+  }
+  LegGridDev leg(bool cplx) const {
+    LegGridDev g;
+    g.k = k;
+    g.n_t = k;
+    g.n_bins = cplx ? N : k;
+    g.cos_t = cos_t;
+    g.sin_t = sin_t;
+    g.ring_w = ring_w;
+    g.act = act;
+    return g;
+  }
+  int n_bins(bool cplx) const { return cplx ? N : k; }
+  // rough cost of the Legendre work for order m (ring-steps)
+  double cost(int m) const {
+    const int2 a = act_host[m];
+    return (double)(k - m) * (double)std::max(0, a.y - a.x) + 64.0;
+  }
+};
+
+static std::map<std::tuple<int, int, int>, GridRes*> g_grids;
+
+template <class T>
+static int upload_new(T** dst, const std::vector<T>& v) {
+  CU(cudaMalloc(dst, std::max<size_t>(16, v.size() * sizeof(T))));
+  if (!v.empty()) CU(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return S2W_OK;
+}
+
+static int get_grid(int dev, int scheme, int k, GridRes** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, scheme, k);
+  auto it = g_grids.find(key);
+  if (it != g_grids.end()) {
+    *out = it->second;
+    return S2W_OK;
+  }
+  if (k < 1 || k >= SEED_KMAX) return fail(S2W_EPARAM, "band-limit %d out of range [1, %d)", k, SEED_KMAX);
+  DeviceTables* dt;
+  CHECK(device_tables(dev, &dt));
+  GridRes* g = new GridRes();
+  g->device = dev;
+  g->scheme = scheme;
+  g->k = k;
+  g->N = 2 * k - 1;
+  g->logM = std::max(3, ilog2_ceil(2LL * g->N - 1));
+  g->seed_c = dt->seed_c;
+  const int N = g->N, M = 1 << g->logM;
+
+  std::vector<double> theta, wq;
+  if (scheme == S2W_SCHEME_GL) gl_nodes(k, theta, wq);
+  else mw_nodes(k, theta);
+  std::vector<double> c(k), s(k), rw(k);
+  for (int t = 0; t < k; ++t) {
+    c[t] = std::cos(theta[t]);
+    s[t] = std::sin(theta[t]);
+    if (scheme == S2W_SCHEME_GL) rw[t] = 2.0 * M_PI * wq[t];
+    else rw[t] = (2.0 * M_PI / (double)N) * (t == k - 1 ? 0.5 : 1.0);
+  }
+  CHECK(upload_new(&g->cos_t, c));
+  CHECK(upload_new(&g->sin_t, s));
+  CHECK(upload_new(&g->ring_w, rw));
+
+  // active ring range per order (probe kernel, once per grid)
+  int* d_mmax = nullptr;
+  CU(cudaMalloc(&d_mmax, sizeof(int) * k));
+  CU(launch_leg_probe(k, k, g->cos_t, g->sin_t, g->seed_c, d_mmax, 0));
+  std::vector<int> mmax(k);
+  CU(cudaMemcpy(mmax.data(), d_mmax, sizeof(int) * k, cudaMemcpyDeviceToHost));
+  cudaFree(d_mmax);
+  g->act_host.assign(k, make_int2(0, 0));
+  for (int m = 0; m < k; ++m) {
+    int lo = -1, hi = -1;
+    for (int t = 0; t < k; ++t)
+      if (mmax[t] >= m) {
+        if (lo < 0) lo = t;
+        hi = t;
+      }
+    g->act_host[m] = (lo < 0) ? make_int2(0, 0) : make_int2(lo, hi + 1);
+  }
+  CHECK(upload_new(&g->act, g->act_host));
+
+  // FFT / Bluestein / theta-stage tables
+  std::vector<double2> tw(M), chirp(N), ph1(N), ph2(N);
+  for (int j = 0; j < M; ++j) {
+    ld ang = -2.0L * PI_L * (ld)j / (ld)M;
+    tw[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
+  }
+  std::vector<cld> cl(N);
+  for (int n = 0; n < N; ++n) {
+    long long r = ((long long)n * n) % (2LL * N);
+    ld ang = -PI_L * (ld)r / (ld)N;
+    cl[n] = cld(std::cos(ang), std::sin(ang));
+    chirp[n] = d2(cl[n]);
+  }
+  std::vector<cld> b(M, cld(0, 0)), cc(M, cld(0, 0)), w(M, cld(0, 0));
+  for (int j = 0; j < N; ++j) {
+    b[j] = std::conj(cl[j]);
+    cc[j] = cl[j];
+    if (j > 0) {
+      b[M - j] = std::conj(cl[j]);
+      cc[M - j] = cl[j];
+    }
+  }
+  for (int p = -(2 * k - 2); p <= 2 * k - 2; ++p) {
+    if (p & 1) continue;
+    w[(p % M + M) % M] = cld(4.0L / (1.0L - (ld)p * (ld)p), 0);
+  }
+  for (int bin = 0; bin < N; ++bin) {
+    const int q = bin < k ? bin : bin - N;
+    ld a1 = -PI_L * (ld)q / (ld)N;
+    ph1[bin] = d2(cl[bin] * cld(std::cos(a1), std::sin(a1)) / (ld)N);
+    ph2[bin] = d2(cld(std::cos(-a1), std::sin(-a1)) * std::conj(cl[bin]));
+  }
+  CHECK(upload_new(&g->tw, tw));
+  CHECK(upload_new(&g->chirp, chirp));
+  CHECK(upload_new(&g->bl_fwd, spectrum_brev(b)));
+  CHECK(upload_new(&g->bl_inv, spectrum_brev(cc)));
+  CHECK(upload_new(&g->wconv, spectrum_brev(w)));
+  CHECK(upload_new(&g->ph1, ph1));
+  CHECK(upload_new(&g->ph2, ph2));
+  g_grids[key] = g;
+  *out = g;
+  return S2W_OK;
+}
+
+// ------------------------------------------------------------------ Legendre launch configs
+static int pick_ns(int n, bool cplx) {
+  const int cap = cplx ? 8 : 16;
+  int ns = 1;
+  while (ns < n && ns < cap) ns *= 2;
+  return ns;
+}
+
+struct SynthCfg {
+  bool built = false;
+  int key[4] = {0, 0, 0, 0};
+  DevBuf grids, sets, items;
+  int n_items = 0, ns = 1, cplx = 1;
+};
+
+struct AnaCfg {
+  bool built = false;
+  int key[4] = {0, 0, 0, 0};
+  DevBuf grids, sets, segs, items;
+  int n_items = 0, ns = 1, cplx = 1;
+};
+
+// A synthesis "group": sets sharing one grid.
+struct SynthGroupSpec {
+  const GridRes* g;
+  std::vector<SynthSet> sets;
+};
+
+static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups, bool cplx) {
+  std::vector<LegGridDev> grids;
+  std::vector<SynthSet> sets;
+  struct It {
+    SynthItem it;
+    double cost;
+  };
+  std::vector<It> items;
+  int maxn = 1;
+  for (auto& gr : groups) maxn = std::max<int>(maxn, (int)gr.sets.size());
+  const int ns = pick_ns(maxn, cplx);
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const auto& gr = groups[gi];
+    grids.push_back(gr.g->leg(cplx));
+    const int base = (int)sets.size();
+    for (auto& s : gr.sets) sets.push_back(s);
+    const int n = (int)gr.sets.size();
+    for (int m = 0; m < gr.g->k; ++m)
+      for (int s0 = 0; s0 < n; s0 += ns) {
+        const int nset = std::min(ns, n - s0);
+        SynthItem it{(int)gi, m, base + s0, nset};
+        items.push_back({it, gr.g->cost(m) * (3.0 + 4.0 * ns)});
+      }
+  }
+  std::stable_sort(items.begin(), items.end(),
+                   [](const It& a, const It& b) { return a.cost > b.cost; });
+  std::vector<SynthItem> its;
+  for (auto& i : items) its.push_back(i.it);
+  CHECK(cfg.grids.upload(grids));
+  CHECK(cfg.sets.upload(sets));
+  CHECK(cfg.items.upload(its));
+  cfg.n_items = (int)its.size();
+  cfg.ns = ns;
+  cfg.cplx = cplx;
+  cfg.built = true;
+  return S2W_OK;
+}
+
+// Analysis: a segment = sets of one grid processed together.  combine != 0
+// means all sets of the segment accumulate into the same output (weighted).
+struct AnaSegSpec {
+  const GridRes* g;
+  std::vector<AnaSet> sets;
+  int combine;
+};
+
+static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool cplx) {
+  // distinct grids
+  std::vector<const GridRes*> gl;
+  for (auto& s : segspecs)
+    if (std::find(gl.begin(), gl.end(), s.g) == gl.end()) gl.push_back(s.g);
+  std::vector<LegGridDev> grids;
+  for (auto* g : gl) grids.push_back(g->leg(cplx));
+  int maxn = 1, kmax = 0;
+  for (auto& s : segspecs) maxn = std::max<int>(maxn, (int)s.sets.size());
+  for (auto* g : gl) kmax = std::max(kmax, g->k);
+  const int ns = pick_ns(maxn, cplx);
+  // split segments wider than ns
+  std::vector<AnaSet> sets;
+  std::vector<AnaSeg> segs0;
+  std::vector<int> seg_grid_k;
+  for (auto& sp : segspecs) {
+    const int gi = (int)(std::find(gl.begin(), gl.end(), sp.g) - gl.begin());
+    const int n = (int)sp.sets.size();
+    for (int s0 = 0; s0 < n; s0 += ns) {
+      AnaSeg sg;
+      sg.grid = gi;
+      sg.set0 = (int)sets.size();
+      sg.nset = std::min(ns, n - s0);
+      sg.combine = sp.combine;
+      for (int i = 0; i < sg.nset; ++i) sets.push_back(sp.sets[s0 + i]);
+      segs0.push_back(sg);
+    }
+  }
+  // items: one per order m, listing every segment whose grid has k > m
+  struct It {
+    AnaItem it;
+    double cost;
+  };
+  std::vector<AnaSeg> segs;
+  std::vector<It> items;
+  for (int m = 0; m < kmax; ++m) {
+    AnaItem it{m, (int)segs.size(), 0};
+    double cost = 0;
+    for (auto& sg : segs0) {
+      const GridRes* g = gl[sg.grid];
+      if (m >= g->k) continue;
+      segs.push_back(sg);
+      ++it.nseg;
+      cost += g->cost(m) * (3.0 + 4.0 * ns);
+    }
+    if (it.nseg) items.push_back({it, cost});
+  }
+  std::stable_sort(items.begin(), items.end(),
+                   [](const It& a, const It& b) { return a.cost > b.cost; });
+  std::vector<AnaItem> its;
+  for (auto& i : items) its.push_back(i.it);
+  CHECK(cfg.grids.upload(grids));
+  CHECK(cfg.sets.upload(sets));
+  CHECK(cfg.segs.upload(segs));
+  CHECK(cfg.items.upload(its));
+  cfg.n_items = (int)its.size();
+  cfg.ns = ns;
+  cfg.cplx = cplx;
+  cfg.built = true;
+  return S2W_OK;
+}
+
+static int run_synth(const SynthCfg& cfg, const double* seed_c, double2* const* bufs,
+                     cudaStream_t st) {
+  LegSynthArgs a;
+  a.grids = cfg.grids.as<LegGridDev>();
+  a.sets = cfg.sets.as<SynthSet>();
+  a.items = cfg.items.as<SynthItem>();
+  a.seed_c = seed_c;
+  a.n_items = cfg.n_items;
+  a.cplx = cfg.cplx;
+  a.ns = cfg.ns;
+  for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
+  CU(launch_leg_synth(a, st));
+  return S2W_OK;
+}
+
+static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs,
+                   cudaStream_t st) {
+  LegAnaArgs a;
+  a.grids = cfg.grids.as<LegGridDev>();
+  a.sets = cfg.sets.as<AnaSet>();
+  a.segs = cfg.segs.as<AnaSeg>();
+  a.items = cfg.items.as<AnaItem>();
+  a.seed_c = seed_c;
+  a.n_items = cfg.n_items;
+  a.cplx = cfg.cplx;
+  a.ns = cfg.ns;
+  for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
+  CU(launch_leg_ana(a, st));
+  return S2W_OK;
+}
+
+// ------------------------------------------------------------------ shared pipeline steps
+// map [n_sets][k][N] -> H [n_sets][mi][k] (m-major; MW: theta stage applied)
+static int forward_rings(const GridRes* g, int n_sets, bool real, const double* map,
+                         double2* G, cudaStream_t st) {
+  PhiFwdArgs pa;
+  pa.T = g->fft();
+  pa.n_sets = n_sets;
+  pa.n_rings = g->k;
+  pa.real = real ? 1 : 0;
+  pa.in = map;
+  pa.out = G;
+  pa.n_bins = g->n_bins(!real);
+  pa.scale = 1.0 / (double)g->N;
+  CU(launch_phi_fwd(pa, st));
+  if (g->scheme == S2W_SCHEME_MW) {
+    ThetaArgs ta;
+    ta.T = g->fft();
+    ta.n_sets = n_sets;
+    ta.k = g->k;
+    ta.n_bins = g->n_bins(!real);
+    ta.in = G;
+    ta.out = G;
+    CU(launch_theta(ta, st));
+  }
+  return S2W_OK;
+}
+
+// G ring-major [n_sets][k][n_bins] -> map [n_sets][k][N]
+static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
+                         cudaStream_t st) {
+  PhiInvArgs pa;
+  pa.T = g->fft();
+  pa.n_sets = n_sets;
+  pa.n_rings = g->k;
+  pa.real = real ? 1 : 0;
+  pa.mw_pole = g->scheme == S2W_SCHEME_MW;
+  pa.in = G;
+  pa.out = map;
+  pa.n_bins = g->n_bins(!real);
+  CU(launch_phi_inv(pa, st));
+  return S2W_OK;
+}
+
+// ------------------------------------------------------------------ SHT plan
+struct s2w_sht_plan {
+  int device, scheme, L;
+  GridRes* g;
+  DevBuf G;
+  SynthCfg syn;
+  AnaCfg ana;
+};
+
+extern "C" {
+
+const char* s2w_version(void) { return S2W_VERSION; }
+const char* s2w_last_error(void) { return g_err.c_str(); }
+
+int s2w_grid_nodes(int scheme, int L, double* theta, double* weights) {
+  if (L < 1) return fail(S2W_EPARAM, "band-limit must be >= 1, got %d", L);
+  if (scheme != S2W_SCHEME_GL && scheme != S2W_SCHEME_MW)
+    return fail(S2W_EPARAM, "unknown sampling scheme %d", scheme);
+  std::vector<double> th, w;
+  if (scheme == S2W_SCHEME_GL) gl_nodes(L, th, w);
+  else mw_nodes(L, th);
+  if (theta) std::memcpy(theta, th.data(), sizeof(double) * L);
+  if (weights && scheme == S2W_SCHEME_GL) std::memcpy(weights, w.data(), sizeof(double) * L);
+  return S2W_OK;
+}
+
+int s2w_assoc_legendre_ring(int L, double theta, double* table, void* stream) {
+  if (L < 1) return fail(S2W_EPARAM, "band-limit must be >= 1, got %d", L);
+  if (L >= SEED_KMAX) return fail(S2W_EPARAM, "band-limit %d too large", L);
+  if (!(theta >= 0.0 && theta <= M_PI))
+    return fail(S2W_EPARAM, "colatitude must lie in [0, pi], got %g", theta);
+  int dev;
+  CU(cudaGetDevice(&dev));
+  DeviceTables* dt;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    CHECK(device_tables(dev, &dt));
+  }
+  CU(launch_leg_table(L, std::cos(theta), std::sin(theta), dt->seed_c, table,
+                      (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+int s2w_sht_plan_create(int scheme, int L, int device, s2w_sht_plan** plan) {
+  if (!plan) return fail(S2W_EPARAM, "null plan pointer");
+  if (L < 1) return fail(S2W_EPARAM, "band-limit must be >= 1, got %d", L);
+  if (scheme != S2W_SCHEME_GL && scheme != S2W_SCHEME_MW)
+    return fail(S2W_EPARAM, "unknown sampling scheme %d", scheme);
+  DeviceGuard dg(device);
+  CU(dg.err);
+  s2w_sht_plan* p = new s2w_sht_plan();
+  p->device = device;
+  p->scheme = scheme;
+  p->L = L;
+  int r = get_grid(device, scheme, L, &p->g);
+  if (r != S2W_OK) {
+    delete p;
+    return r;
+  }
+  *plan = p;
+  return S2W_OK;
+}
+
+int s2w_sht_plan_destroy(s2w_sht_plan* plan) {
+  if (!plan) return S2W_OK;
+  DeviceGuard dg(plan->device);
+  delete plan;
+  return S2W_OK;
+}
+
+int s2w_sh_synthesis(s2w_sht_plan* p, int n_sets, int L_coef, int is_real, const double* flm,
+                     double* map, void* stream) {
+  if (!p) return fail(S2W_EPARAM, "null plan");
+  if (n_sets < 0) return fail(S2W_EPARAM, "negative set count");
+  if (L_coef < 1 || L_coef > p->L)
+    return fail(S2W_EPARAM, "coefficient band-limit %d exceeds the grid band-limit %d", L_coef,
+                p->L);
+  if (n_sets == 0) return S2W_OK;
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool cplx = !is_real;
+  const GridRes* g = p->g;
+  const int k = g->k, nb = g->n_bins(cplx);
+  CHECK(p->G.ensure(sizeof(double2) * (size_t)n_sets * nb * k));
+  SynthCfg& c = p->syn;
+  if (!c.built || c.key[0] != n_sets || c.key[1] != is_real || c.key[2] != L_coef) {
+    SynthGroupSpec gs;
+    gs.g = g;
+    for (int s = 0; s < n_sets; ++s) {
+      SynthSet ss;
+      ss.fb = 0;
+      ss.foff = (long long)s * L_coef * L_coef;
+      ss.f_L = L_coef;
+      ss.w = nullptr;
+      ss.ob = 1;
+      ss.ooff = (long long)s * nb * k;
+      gs.sets.push_back(ss);
+    }
+    CHECK(build_synth(c, {gs}, cplx));
+    c.key[0] = n_sets;
+    c.key[1] = is_real;
+    c.key[2] = L_coef;
+  }
+  double2* bufs[S2W_NBUF] = {(double2*)flm, p->G.as<double2>(), nullptr, nullptr};
+  CHECK(run_synth(c, g->seed_c, bufs, st));
+  CHECK(inverse_rings(g, n_sets, !cplx, p->G.as<double2>(), map, st));
+  return S2W_OK;
+}
+
+int s2w_sh_analysis(s2w_sht_plan* p, int n_sets, int is_real, const double* map, double* flm,
+                    void* stream) {
+  if (!p) return fail(S2W_EPARAM, "null plan");
+  if (n_sets < 0) return fail(S2W_EPARAM, "negative set count");
+  if (n_sets == 0) return S2W_OK;
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool cplx = !is_real;
+  const GridRes* g = p->g;
+  const int k = g->k, nb = g->n_bins(cplx);
+  CHECK(p->G.ensure(sizeof(double2) * (size_t)n_sets * nb * k));
+  AnaCfg& c = p->ana;
+  if (!c.built || c.key[0] != n_sets || c.key[1] != is_real) {
+    AnaSegSpec sp;
+    sp.g = g;
+    sp.combine = 0;
+    for (int s = 0; s < n_sets; ++s) {
+      AnaSet as;
+      as.hb = 1;
+      as.hoff = (long long)s * nb * k;
+      as.ob = 0;
+      as.ooff = (long long)s * k * k;
+      as.w = nullptr;
+      sp.sets.push_back(as);
+    }
+    CHECK(build_ana(c, {sp}, cplx));
+    c.key[0] = n_sets;
+    c.key[1] = is_real;
+  }
+  CHECK(forward_rings(g, n_sets, !cplx, map, p->G.as<double2>(), st));
+  CU(cudaMemsetAsync(flm, 0, sizeof(double2) * (size_t)n_sets * k * k, st));
+  double2* bufs[S2W_NBUF] = {(double2*)flm, p->G.as<double2>(), nullptr, nullptr};
+  CHECK(run_ana(c, g->seed_c, bufs, st));
+  return S2W_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ wavelet plan
+struct s2w_wav_plan {
+  int device, scheme, L, B, real, nk;
+  std::vector<int> bands;
+  DevBuf fac;                         // [nk][L]
+  GridRes* top = nullptr;             // grid at L
+  std::vector<GridRes*> kgrid;        // grid per kernel index
+  std::vector<long long> goff;        // offset (double2) of scale j's G block in Gs
+  DevBuf f, Gtop, Gs;
+  SynthCfg syn_top, syn_scales;
+  AnaCfg ana_top, ana_scales;
+  double2* bufs() const { return nullptr; }
+};
+
+extern "C" {
+
+int s2w_wav_plan_create(int scheme, int L, int batch, int is_real, int n_kern,
+                        const double* kernels, const int* bands, int device,
+                        s2w_wav_plan** plan) {
+  if (!plan || !kernels || !bands) return fail(S2W_EPARAM, "null argument");
+  if (L < 2) return fail(S2W_EPARAM, "band-limit must be >= 2 for a wavelet tiling, got %d", L);
+  if (batch < 1) return fail(S2W_EPARAM, "batch must be >= 1");
+  if (n_kern < 1 || n_kern > S2W_MAXK)
+    return fail(S2W_EPARAM, "kernel count %d out of range [1, %d]", n_kern, S2W_MAXK);
+  if (scheme != S2W_SCHEME_GL && scheme != S2W_SCHEME_MW)
+    return fail(S2W_EPARAM, "unknown sampling scheme %d", scheme);
+  for (int j = 0; j < n_kern; ++j)
+    if (bands[j] < 1 || bands[j] > L)
+      return fail(S2W_EPARAM, "scale band-limit %d outside [1, %d]", bands[j], L);
+  DeviceGuard dg(device);
+  CU(dg.err);
+  s2w_wav_plan* p = new s2w_wav_plan();
+  p->device = device;
+  p->scheme = scheme;
+  p->L = L;
+  p->B = batch;
+  p->real = is_real ? 1 : 0;
+  p->nk = n_kern;
+  p->bands.assign(bands, bands + n_kern);
+  auto bail = [&](int r) {
+    delete p;
+    return r;
+  };
+  // tiling factors sqrt(4 pi / (2l+1)) * K_j(l)  (transform.py:117-126)
+  std::vector<double> fac((size_t)n_kern * L);
+  for (int j = 0; j < n_kern; ++j)
+    for (int l = 0; l < L; ++l)
+      fac[(size_t)j * L + l] = std::sqrt(4.0 * M_PI / (2.0 * l + 1.0)) * kernels[(size_t)j * L + l];
+  int r;
+  if ((r = p->fac.upload(fac)) != S2W_OK) return bail(r);
+  if ((r = get_grid(device, scheme, L, &p->top)) != S2W_OK) return bail(r);
+  const bool cplx = !is_real;
+  long long off = 0;
+  for (int j = 0; j < n_kern; ++j) {
+    GridRes* g;
+    if ((r = get_grid(device, scheme, bands[j], &g)) != S2W_OK) return bail(r);
+    p->kgrid.push_back(g);
+    p->goff.push_back(off);
+    off += (long long)batch * g->n_bins(cplx) * g->k;
+  }
+  if ((r = p->f.ensure(sizeof(double2) * (size_t)batch * L * L)) != S2W_OK) return bail(r);
+  if ((r = p->Gtop.ensure(sizeof(double2) * (size_t)batch * p->top->n_bins(cplx) * L)) != S2W_OK)
+    return bail(r);
+  if ((r = p->Gs.ensure(sizeof(double2) * (size_t)off)) != S2W_OK) return bail(r);
+
+  // slots: 0 = f, 1 = Gtop, 2 = Gs
+  const int nbL = p->top->n_bins(cplx);
+  // (a) analysis at L into f (plain)
+  {
+    AnaSegSpec sp;
+    sp.g = p->top;
+    sp.combine = 0;
+    for (int b = 0; b < batch; ++b)
+      sp.sets.push_back(AnaSet{1, (long long)b * nbL * L, 0, (long long)b * L * L, nullptr});
+    if ((r = build_ana(p->ana_top, {sp}, cplx)) != S2W_OK) return bail(r);
+  }
+  // (b) synthesis at L from f (plain)
+  {
+    SynthGroupSpec gs;
+    gs.g = p->top;
+    for (int b = 0; b < batch; ++b)
+      gs.sets.push_back(SynthSet{0, (long long)b * L * L, L, nullptr, 1, (long long)b * nbL * L});
+    if ((r = build_synth(p->syn_top, {gs}, cplx)) != S2W_OK) return bail(r);
+  }
+  // distinct scale grids (ascending band)
+  std::vector<int> distinct(p->bands);
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  // (c) grouped per-scale synthesis: f * fac_j, truncated to band_j
+  {
+    std::vector<SynthGroupSpec> groups;
+    for (int kb : distinct) {
+      SynthGroupSpec gs;
+      for (int j = 0; j < n_kern; ++j) {
+        if (p->bands[j] != kb) continue;
+        gs.g = p->kgrid[j];
+        const int nb = gs.g->n_bins(cplx);
+        for (int b = 0; b < batch; ++b)
+          gs.sets.push_back(SynthSet{0, (long long)b * L * L, L, p->fac.as<double>() + (size_t)j * L,
+                                     2, p->goff[j] + (long long)b * nb * kb});
+      }
+      groups.push_back(gs);
+    }
+    if ((r = build_synth(p->syn_scales, groups, cplx)) != S2W_OK) return bail(r);
+  }
+  // (d) grouped per-scale analysis recombined into f (weighted by fac_j)
+  {
+    std::vector<AnaSegSpec> segs;
+    for (int kb : distinct) {
+      std::vector<int> js;
+      for (int j = 0; j < n_kern; ++j)
+        if (p->bands[j] == kb) js.push_back(j);
+      const GridRes* g = p->kgrid[js[0]];
+      const int nb = g->n_bins(cplx);
+      if ((int)js.size() > 1 && batch == 1) {
+        // one output, several weighted scales: share the recursion
+        AnaSegSpec sp;
+        sp.g = g;
+        sp.combine = 1;
+        for (int j : js)
+          sp.sets.push_back(AnaSet{2, p->goff[j], 0, 0, p->fac.as<double>() + (size_t)j * L});
+        segs.push_back(sp);
+      } else {
+        for (int j : js) {
+          AnaSegSpec sp;
+          sp.g = g;
+          sp.combine = 0;
+          for (int b = 0; b < batch; ++b)
+            sp.sets.push_back(AnaSet{2, p->goff[j] + (long long)b * nb * kb, 0, (long long)b * L * L,
+                                     p->fac.as<double>() + (size_t)j * L});
+          segs.push_back(sp);
+        }
+      }
+    }
+    if ((r = build_ana(p->ana_scales, segs, cplx)) != S2W_OK) return bail(r);
+  }
+  *plan = p;
+  return S2W_OK;
+}
+
+int s2w_wav_plan_destroy(s2w_wav_plan* plan) {
+  if (!plan) return S2W_OK;
+  DeviceGuard dg(plan->device);
+  delete plan;
+  return S2W_OK;
+}
+
+int s2w_wav_plan_flm(s2w_wav_plan* p, double** flm) {
+  if (!p || !flm) return fail(S2W_EPARAM, "null argument");
+  *flm = p->f.as<double>();
+  return S2W_OK;
+}
+
+int s2w_wav_analysis_harmonic(s2w_wav_plan* p, int truncate, const double* flm,
+                              double* const* outs, void* stream) {
+  if (!p || !flm || !outs) return fail(S2W_EPARAM, "null argument");
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  TileArgs a;
+  a.n_sets = p->B;
+  a.L = p->L;
+  a.n_k = p->nk;
+  a.fac = p->fac.as<double>();
+  for (int j = 0; j < p->nk; ++j) {
+    a.band[j] = truncate ? p->bands[j] : p->L;
+    a.ptr[j] = (double2*)outs[j];
+  }
+  a.f_in = (const double2*)flm;
+  a.f_out = nullptr;
+  CU(launch_tile_analysis(a, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+int s2w_wav_synthesis_harmonic(s2w_wav_plan* p, int full_band, const double* const* ins,
+                               double* flm, void* stream) {
+  if (!p || !flm || !ins) return fail(S2W_EPARAM, "null argument");
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  TileArgs a;
+  a.n_sets = p->B;
+  a.L = p->L;
+  a.n_k = p->nk;
+  a.fac = p->fac.as<double>();
+  for (int j = 0; j < p->nk; ++j) {
+    a.band[j] = full_band ? p->L : p->bands[j];
+    a.ptr[j] = (double2*)ins[j];
+  }
+  a.f_in = nullptr;
+  a.f_out = (double2*)flm;
+  CU(launch_tile_synthesis(a, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+int s2w_wav_analysis_pixel(s2w_wav_plan* p, const double* map, double* const* scale_maps,
+                           void* stream) {
+  if (!p || !map || !scale_maps) return fail(S2W_EPARAM, "null argument");
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool cplx = !p->real;
+  double2* bufs[S2W_NBUF] = {p->f.as<double2>(), p->Gtop.as<double2>(), p->Gs.as<double2>(),
+                             nullptr};
+  // sh_analysis at L (transform.py:186)
+  CHECK(forward_rings(p->top, p->B, !cplx, map, p->Gtop.as<double2>(), st));
+  CU(cudaMemsetAsync(p->f.p, 0, sizeof(double2) * (size_t)p->B * p->L * p->L, st));
+  CHECK(run_ana(p->ana_top, p->top->seed_c, bufs, st));
+  // tiling + truncation fused into the grouped per-scale synthesis (transform.py:187-190)
+  CHECK(run_synth(p->syn_scales, p->top->seed_c, bufs, st));
+  for (int j = 0; j < p->nk; ++j)
+    CHECK(inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
+                        st));
+  return S2W_OK;
+}
+
+int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, double* map,
+                            void* stream) {
+  if (!p || !map || !scale_maps) return fail(S2W_EPARAM, "null argument");
+  DeviceGuard dg(p->device);
+  CU(dg.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool cplx = !p->real;
+  double2* bufs[S2W_NBUF] = {p->f.as<double2>(), p->Gtop.as<double2>(), p->Gs.as<double2>(),
+                             nullptr};
+  // per-scale analysis (transform.py:196)
+  for (int j = 0; j < p->nk; ++j)
+    CHECK(forward_rings(p->kgrid[j], p->B, !cplx, scale_maps[j], p->Gs.as<double2>() + p->goff[j],
+                        st));
+  CU(cudaMemsetAsync(p->f.p, 0, sizeof(double2) * (size_t)p->B * p->L * p->L, st));
+  // recombination (transform.py:197-199) fused into the analysis reduction
+  CHECK(run_ana(p->ana_scales, p->top->seed_c, bufs, st));
+  // sh_synthesis at L (transform.py:200)
+  CHECK(run_synth(p->syn_top, p->top->seed_c, bufs, st));
+  CHECK(inverse_rings(p->top, p->B, !cplx, p->Gtop.as<double2>(), map, st));
+  return S2W_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// Ring (phi) FFT and MW theta-stage kernels.
+//
+//  phi_fwd_kernel : map rows (theta-major) -> G_m(theta_t) = DFT_N(row)/N, written
+//                   m-major ([mi][t]) so the theta stage and the Legendre
+//                   analysis read contiguous columns.  Replaces the np.fft.fft /
+//                   rfft calls of sh_analysis_stack (sht.py:322,335).
+//  phi_inv_kernel : G ring-major ([t][mi]) -> map rows, unnormalised inverse DFT
+//                   (np.fft.ifft/irfft with norm="forward", sht.py:266-273), plus the
+//                   MW south-pole pinning of sht.py:274-279.
+//  theta_kernel   : MW forward theta stage per order m (absent from the reference,
+//                   whose MW analysis raises at sht.py:300-303): parity extension to
+//                   the full circle, DFT_N, convolution with the Fourier series of
+//                   |sin theta|, inverse DFT_N on the first L rings.  See DESIGN.md.
+//
+// All odd-length DFTs (N = 2L-1) are Bluestein chirp-z transforms over the
+// power-of-two shared-memory FFT in fft.cuh.
+#include "fft.cuh"
+#include "s2w_internal.h"
+
+namespace s2w {
+
+__device__ __forceinline__ double2 load_map_elem(const double* __restrict__ in, long long idx,
+                                                 int real) {
+  if (real) return make_double2(__ldg(&in[idx]), 0.0);
+  return __ldg(reinterpret_cast<const double2*>(in) + idx);
+}
+
+// ---------------------------------------------------------------- phi forward
+__global__ void phi_fwd_kernel(PhiFwdArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int M = 1 << T.logM, N = T.N;
+  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  double2* buf = smem + (size_t)grp * M;
+  const int row = blockIdx.x * a.rpc + grp;
+  const int n_rows = a.n_sets * a.n_rings;
+  const bool valid = row < n_rows;
+  const int set = valid ? row / a.n_rings : 0;
+  const int t = valid ? row - set * a.n_rings : 0;
+  const long long in_base = ((long long)set * a.n_rings + t) * N;
+
+  for (int n = gtid; n < M; n += a.gsize) {
+    double2 v = make_double2(0.0, 0.0);
+    if (valid && n < N) v = cmul(load_map_elem(a.in, in_base + n, a.real), __ldg(&T.chirp[n]));
+    buf[swz(n)] = v;
+  }
+  __syncthreads();
+  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
+  __syncthreads();
+  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  if (!valid) return;
+  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
+  for (int mi = gtid; mi < a.n_bins; mi += a.gsize) {
+    double2 v = cscale(cmul(__ldg(&T.chirp[mi]), buf[swz(mi)]), a.scale);
+    out[(size_t)mi * a.n_rings + t] = v;
+  }
+}
+
+// ---------------------------------------------------------------- phi inverse
+__global__ void phi_inv_kernel(PhiInvArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int M = 1 << T.logM, N = T.N;
+  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  double2* buf = smem + (size_t)grp * M;
+  const int row = blockIdx.x * a.rpc + grp;
+  const int n_rows = a.n_sets * a.n_rings;
+  const bool valid = row < n_rows;
+  const int set = valid ? row / a.n_rings : 0;
+  const int t = valid ? row - set * a.n_rings : 0;
+  const double2* G = a.in + ((size_t)set * a.n_rings + t) * a.n_bins;
+
+  for (int n = gtid; n < M; n += a.gsize) {
+    double2 v = make_double2(0.0, 0.0);
+    if (valid && n < N) {
+      if (!a.real) {
+        v = __ldg(&G[n]);
+      } else if (n < a.n_bins) {
+        v = __ldg(&G[n]);
+        if (n == 0) v.y = 0.0;  // irfft ignores Im of the DC bin
+      } else {
+        v = cconj(__ldg(&G[N - n]));
+      }
+      v = cmulc(v, __ldg(&T.chirp[n]));
+    }
+    buf[swz(n)] = v;
+  }
+  __syncthreads();
+  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
+  __syncthreads();
+  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  if (!valid) return;
+  const bool pole = a.mw_pole && t == a.n_rings - 1;
+  double2 pv = make_double2(0.0, 0.0);
+  if (pole) pv = __ldg(&G[0]);
+  const size_t ob = ((size_t)set * a.n_rings + t) * N;
+  if (a.real) {
+    double* out = a.out + ob;
+    for (int p = gtid; p < N; p += a.gsize)
+      out[p] = pole ? pv.x : cmulc(buf[swz(p)], __ldg(&T.chirp[p])).x;
+  } else {
+    double2* out = reinterpret_cast<double2*>(a.out) + ob;
+    for (int p = gtid; p < N; p += a.gsize)
+      out[p] = pole ? pv : cmulc(buf[swz(p)], __ldg(&T.chirp[p]));
+  }
+}
+
+// ---------------------------------------------------------------- MW theta stage
+__global__ void theta_kernel(ThetaArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int M = 1 << T.logM, N = T.N, k = a.k;
+  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  double2* buf = smem + (size_t)grp * M;
+  const int row = blockIdx.x * a.rpc + grp;
+  const int n_rows = a.n_sets * a.n_bins;
+  const bool valid = row < n_rows;
+  const int set = valid ? row / a.n_bins : 0;
+  const int mi = valid ? row - set * a.n_bins : 0;
+  const int m = (mi < k) ? mi : mi - N;
+  const double sgn = (m & 1) ? -1.0 : 1.0;
+  const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
+
+  // 1. parity extension to the full circle, times the Bluestein chirp
+  for (int n = gtid; n < M; n += a.gsize) {
+    double2 v = make_double2(0.0, 0.0);
+    if (valid && n < N) {
+      v = (n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn);
+      v = cmul(v, __ldg(&T.chirp[n]));
+    }
+    buf[swz(n)] = v;
+  }
+  __syncthreads();
+  // 2. DFT_N (Bluestein)
+  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
+  __syncthreads();
+  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  // 3. Fourier coefficients a_{m'} = c_bin e^{-i pi m'/N} conv[bin] / N, laid out
+  //    over the length-M circle (negative m' at the top)
+  for (int bin = gtid; bin < N; bin += a.gsize) {
+    double2 v = cmul(buf[swz(bin)], __ldg(&T.ph1[bin]));
+    if (bin < k) buf[swz(bin)] = v;
+    else buf[swz(M - N + bin)] = v;
+  }
+  __syncthreads();
+  for (int n = k + gtid; n < M - k + 1; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 4. convolution with the |sin theta| series (precomputed spectrum)
+  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  pointwise_mul(buf, M, T.wconv, gtid, a.gsize);
+  __syncthreads();
+  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  // 5. back onto N bins with the e^{i pi q/N} offset phase and the inverse chirp
+  for (int bin = gtid; bin < N; bin += a.gsize) {
+    double2 v = (bin < k) ? buf[swz(bin)] : buf[swz(M - N + bin)];
+    v = cmul(v, __ldg(&T.ph2[bin]));
+    buf[swz(bin)] = v;  // bins >= k read from [M-k+1, M), disjoint from [k, N)
+  }
+  __syncthreads();
+  for (int n = N + gtid; n < M; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 6. inverse DFT_N (Bluestein), keep the first k rings
+  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
+  __syncthreads();
+  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  if (!valid) return;
+  double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
+  for (int t = gtid; t < k; t += a.gsize) H[t] = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
+}
+
+// ---------------------------------------------------------------- launchers
+static void fft_geometry(int logM, int max_rows_smem, int& gsize, int& rpc, size_t& smem) {
+  const int M = 1 << logM;
+  gsize = M / 8;
+  if (gsize > 512) gsize = 512;
+  if (gsize < 1) gsize = 1;
+  rpc = 1;
+  while (rpc * gsize < 128 && (size_t)(rpc * 2) * M * sizeof(double2) <= 64 * 1024 &&
+         rpc * 2 <= max_rows_smem)
+    rpc *= 2;
+  smem = (size_t)rpc * M * sizeof(double2);
+}
+
+static cudaError_t set_smem(const void* fn, size_t smem) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
+  const int n_rows = a.n_sets * a.n_rings;
+  if (n_rows == 0) return cudaSuccess;
+  size_t smem;
+  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
+  cudaError_t e = set_smem((const void*)phi_fwd_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (n_rows + a.rpc - 1) / a.rpc;
+  phi_fwd_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
+  const int n_rows = a.n_sets * a.n_rings;
+  if (n_rows == 0) return cudaSuccess;
+  size_t smem;
+  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
+  cudaError_t e = set_smem((const void*)phi_inv_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (n_rows + a.rpc - 1) / a.rpc;
+  phi_inv_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
+  const int n_rows = a.n_sets * a.n_bins;
+  if (n_rows == 0) return cudaSuccess;
+  size_t smem;
+  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
+  cudaError_t e = set_smem((const void*)theta_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (n_rows + a.rpc - 1) / a.rpc;
+  theta_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace s2w

@@ -1,0 +1,147 @@
+// Internal (non-ABI) declarations shared by the s2w CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace s2w {
+
+// ------------------------------------------------------------------ FFT tables
+// Per grid band k (N = 2k-1, M = 2^logM >= 2N-1).  All spectra are stored in
+// bit-reversed order (see fft.cuh) and carry the 1/M of the unnormalised
+// inverse FFT.
+struct FftTablesDev {
+  int N, logM;
+  const double2* tw;      // [M]  exp(-2 pi i j/M)
+  const double2* chirp;   // [N]  c_n = exp(-i pi n^2/N)
+  const double2* bl_fwd;  // [M]  FFT(conj c, circular)/M
+  const double2* bl_inv;  // [M]  FFT(c, circular)/M
+  const double2* ph1;     // [N]  c_b exp(-i pi m'(b)/N)/N      (MW theta stage)
+  const double2* ph2;     // [N]  exp(i pi q(b)/N) conj(c_b)    (MW theta stage)
+  const double2* wconv;   // [M]  FFT(w_hat, circular)/M, w_hat(p)=4/(1-p^2) p even
+};
+
+struct PhiFwdArgs {
+  FftTablesDev T;
+  int n_sets, n_rings, real;
+  const double* in;  // [set][ring][N] real doubles or interleaved complex
+  double2* out;      // [set][mi][ring], mi < n_bins
+  int n_bins;
+  double scale;
+  int gsize, rpc;  // filled by the launcher
+};
+
+struct PhiInvArgs {
+  FftTablesDev T;
+  int n_sets, n_rings, real, mw_pole;
+  const double2* in;  // [set][ring][n_bins]
+  double* out;        // [set][ring][N]
+  int n_bins;
+  int gsize, rpc;
+};
+
+struct ThetaArgs {
+  FftTablesDev T;
+  int n_sets, k, n_bins;
+  const double2* in;  // [set][mi][k]
+  double2* out;       // [set][mi][k] (may alias in)
+  int gsize, rpc;
+};
+
+cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
+cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st);
+cudaError_t launch_theta(ThetaArgs a, cudaStream_t st);
+
+// ------------------------------------------------------------------ Legendre
+struct LegGridDev {
+  int k;       // band limit of the grid = number of orders / degrees
+  int n_t;     // number of rings
+  int n_bins;  // azimuthal bins stored per ring: 2k-1 (complex) or k (real)
+  const double* cos_t;
+  const double* sin_t;
+  const double* ring_w;  // analysis quadrature weight per ring (incl. 2 pi / N factors)
+  const int2* act;       // [k] active ring range [lo, hi) per order m
+};
+
+// Buffers are addressed as (slot, element offset) into the per-launch base
+// table LegSynthArgs::bufs / LegAnaArgs::bufs, so descriptor arrays stay
+// device-resident across calls while user pointers change.
+constexpr int S2W_NBUF = 4;
+
+struct SynthSet {
+  int fb;            // source coefficients: flat l^2+l+m layout, band f_L
+  long long foff;
+  int f_L;
+  const double* w;   // per-degree real weight (tiling factor) or nullptr
+  int ob;            // output G, ring-major [t][n_bins]
+  long long ooff;
+};
+
+struct SynthItem {
+  int grid, m, set0, nset;
+};
+
+struct AnaSet {
+  int hb;            // input H, m-major [mi][t], n_bins rows of n_t
+  long long hoff;
+  int ob;            // output flat l^2+l+m, accumulated (+=)
+  long long ooff;
+  const double* w;   // per-degree weight or nullptr
+};
+
+struct AnaSeg {
+  int grid, set0, nset;
+  int combine;  // all sets accumulate (weighted) into the output of set0
+};
+
+struct AnaItem {
+  int m, seg0, nseg;
+};
+
+struct LegSynthArgs {
+  const LegGridDev* grids;
+  const SynthSet* sets;
+  const SynthItem* items;
+  const double* seed_c;  // [kmax] c_m
+  int n_items;
+  int cplx;
+  int ns;  // compile-time set width selected by the launcher
+  double2* bufs[S2W_NBUF];
+};
+
+struct LegAnaArgs {
+  const LegGridDev* grids;
+  const AnaSet* sets;
+  const AnaSeg* segs;
+  const AnaItem* items;
+  const double* seed_c;
+  int n_items;
+  int cplx;
+  int ns;
+  double2* bufs[S2W_NBUF];
+};
+
+cudaError_t launch_leg_synth(const LegSynthArgs& a, cudaStream_t st);
+cudaError_t launch_leg_ana(const LegAnaArgs& a, cudaStream_t st);
+// Per ring: largest order m whose Legendre column reaches the significance
+// threshold below degree k (used to build the per-m active ring ranges).
+cudaError_t launch_leg_probe(int k, int n_t, const double* cos_t, const double* sin_t,
+                             const double* seed_c, int* mmax_out, cudaStream_t st);
+// Table of orthonormal P_lm(cos theta) for one theta: out[l*L+m] (assoc_legendre_ring).
+cudaError_t launch_leg_table(int L, double cos_t, double sin_t, const double* seed_c,
+                             double* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ tiling
+constexpr int S2W_MAXK = 64;
+struct TileArgs {
+  int n_sets, L, n_k;
+  const double* fac;        // [n_k][L]  sqrt(4pi/(2l+1)) K_j(l)
+  int band[S2W_MAXK];       // coefficient band of each per-kernel set
+  double2* ptr[S2W_MAXK];   // analysis: outputs; synthesis: inputs
+  const double2* f_in;      // analysis input  [set][L^2]
+  double2* f_out;           // synthesis output [set][L^2]
+};
+// out_j[set][i] = f[set][i] * fac_j[l(i)] for i < band_j^2   (transform.py:117-150)
+cudaError_t launch_tile_analysis(const TileArgs& a, cudaStream_t st);
+// f[set][i] = sum_j fac_j[l] * in_j[set][i] (i < band_j^2), j ascending (transform.py:153-172)
+cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st);
+
+}  // namespace s2w

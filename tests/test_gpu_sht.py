@@ -1,0 +1,147 @@
+"""GPU parity of the SHT path against reference golden vectors.
+
+Golden maps were produced by the reference's own sh_synthesis / sh_analysis
+(tests/golden/make_golden.py).  Tolerance: 1e-10 normwise relative (the
+north-star bar), plus the reference's own KAT tolerances where stricter.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+LS = (1, 2, 4, 5, 7, 8, 16, 24, 33, 64)
+
+
+@pytest.fixture(scope="module")
+def sw():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1211_1680_b200 as m
+
+    return m
+
+
+def coeffs(sw, g, L, real):
+    tag = f"L{L}_{'r' if real else 'c'}"
+    return sw.HarmonicCoeffs(L, g(f"sht_small")[f"f_{tag}"], real_signal=real), tag
+
+
+@pytest.mark.parametrize("L", LS)
+@pytest.mark.parametrize("real", [True, False])
+@pytest.mark.parametrize("scheme", ["GL", "MW"])
+def test_synthesis_matches_reference(sw, golden, L, real, scheme):
+    f, tag = coeffs(sw, golden, L, real)
+    grid = sw.make_grid(getattr(sw.SamplingScheme, scheme), L)
+    m = sw.sh_synthesis(f, grid)
+    ref = golden("sht_small")[f"{scheme.lower()}_map_{tag}"]
+    assert rel_err(m.values, ref) <= TOL
+    assert m.is_real == real
+    if real:
+        assert np.all(m.values.imag == 0.0)
+    if scheme == "MW":
+        assert np.all(m.values[-1] == m.values[-1, 0])
+
+
+@pytest.mark.parametrize("L", LS)
+@pytest.mark.parametrize("real", [True, False])
+def test_gl_analysis_matches_reference(sw, golden, L, real):
+    f, tag = coeffs(sw, golden, L, real)
+    grid = sw.make_grid(sw.SamplingScheme.GL, L)
+    smap = sw.SphereMap(grid, golden("sht_small")[f"gl_map_{tag}"], is_real=real)
+    out = sw.sh_analysis(smap)
+    assert rel_err(out.coeffs, golden("sht_small")[f"gl_ana_{tag}"]) <= TOL
+    assert np.abs(out.coeffs - f.coeffs).max() <= 1e-10
+    assert out.real_signal == real
+
+
+@pytest.mark.parametrize("L", LS)
+@pytest.mark.parametrize("real", [True, False])
+def test_mw_analysis_recovers_reference_coefficients(sw, golden, L, real):
+    """MW forward transform (absent in the reference): analysing the reference's
+    own MW synthesis must return the seeded f_lm."""
+    f, tag = coeffs(sw, golden, L, real)
+    grid = sw.make_grid(sw.SamplingScheme.MW, L)
+    smap = sw.SphereMap(grid, golden("sht_small")[f"mw_map_{tag}"], is_real=real)
+    out = sw.sh_analysis(smap)
+    assert np.abs(out.coeffs - f.coeffs).max() <= 1e-10
+    assert out.real_signal == real
+
+
+def test_upsampled_synthesis(sw, golden):
+    g = golden("sht_small")
+    f = sw.HarmonicCoeffs(6, g["f_up6"], real_signal=True)
+    for scheme in ("GL", "MW"):
+        m = sw.sh_synthesis(f, sw.make_grid(getattr(sw.SamplingScheme, scheme), 13))
+        assert rel_err(m.values, g[f"{scheme.lower()}_map_up6_13"]) <= TOL
+        back = sw.truncate_coeffs(sw.sh_analysis(m), 6)
+        assert np.abs(back.coeffs - f.coeffs).max() <= 1e-12
+
+
+def test_constant_and_closed_forms(sw):
+    L = 4
+    c = np.zeros(L * L, complex)
+    c[0] = math.sqrt(4 * math.pi)
+    for scheme in (sw.SamplingScheme.GL, sw.SamplingScheme.MW):
+        m = sw.sh_synthesis(sw.HarmonicCoeffs(L, c, real_signal=True), sw.make_grid(scheme, L))
+        np.testing.assert_allclose(m.values.real, 1.0, atol=1e-14)
+        flm = sw.sh_analysis(sw.map_constant(sw.make_grid(scheme, 8), 1.0))
+        assert abs(flm.coeffs[0] - math.sqrt(4 * math.pi)) <= 1e-13
+        assert np.abs(flm.coeffs[1:]).max() <= 1e-12
+    # Y21 closed form (test_sht.py:46-51 KAT)
+    grid = sw.make_grid(sw.SamplingScheme.GL, 4)
+    d = np.zeros(16, complex)
+    d[sw.lm_index(2, 1)] = 1.0
+    m = sw.sh_synthesis(sw.HarmonicCoeffs(4, d), grid)
+    th, ph = np.meshgrid(grid.theta_nodes, grid.phis, indexing="ij")
+    y21 = -math.sqrt(15 / (8 * math.pi)) * np.sin(th) * np.cos(th) * np.exp(1j * ph)
+    assert np.abs(m.values - y21).max() <= 1e-14
+
+
+@pytest.mark.parametrize("scheme", ["GL", "MW"])
+@pytest.mark.parametrize("real", [True, False])
+@pytest.mark.parametrize("L", [2, 3, 7, 32, 100, 128, 256])
+def test_round_trip(sw, scheme, real, L):
+    rng = np.random.default_rng(L + 17 * real)
+    f = sw.gaussian_coeffs(L, rng, real_signal=real)
+    grid = sw.make_grid(getattr(sw.SamplingScheme, scheme), L)
+    rec = sw.sh_analysis(sw.sh_synthesis(f, grid))
+    assert np.abs(rec.coeffs - f.coeffs).max() <= 1e-10
+    assert rec.real_signal == real
+
+
+def test_stack_matches_single(sw):
+    rng = np.random.default_rng(3)
+    grid = sw.make_grid(sw.SamplingScheme.MW, 40)
+    fs = [sw.gaussian_coeffs(40, rng, real_signal=False) for _ in range(5)]
+    maps = sw.sh_synthesis_stack(fs, grid)
+    for f, m in zip(fs, maps):
+        assert np.array_equal(m.values, sw.sh_synthesis(f, grid).values)
+    outs = sw.sh_analysis_stack(maps)
+    for f, o in zip(fs, outs):
+        assert np.abs(o.coeffs - f.coeffs).max() <= 1e-11
+
+
+def test_deterministic(sw):
+    rng = np.random.default_rng(9)
+    f = sw.gaussian_coeffs(96, rng, real_signal=False)
+    grid = sw.make_grid(sw.SamplingScheme.MW, 96)
+    a = sw.sh_analysis(sw.sh_synthesis(f, grid)).coeffs
+    b = sw.sh_analysis(sw.sh_synthesis(f, grid)).coeffs
+    assert np.array_equal(a, b)
+
+
+def test_legendre_ring(sw, golden):
+    g = golden("legendre")
+    assert rel_err(sw.assoc_legendre_ring(16, 1.0), g["ring_L16_t1"]) <= 1e-13
+    assert rel_err(sw.assoc_legendre_ring(40, 0.3), g["ring_L40_t03"]) <= 1e-13
+    assert rel_err(sw.assoc_legendre_ring(1536, 0.7)[::97], g["ring_L1536_t07_rows"]) <= 1e-12
+    big = sw.assoc_legendre_ring(4096, 0.7)
+    assert np.all(np.isfinite(big))
+    assert np.abs(big).max() <= math.sqrt((2 * 4096 - 1) / (4 * math.pi)) * 1.01
