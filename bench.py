@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark: wavelet analysis+synthesis round trips/s (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config C4 -- L=2048 MW sampling, one complex
+map with f_lm ~ Gaussian, C_l = (l+1)^-2, lambda=3, J0=2, multiresolution.
+One step = one wavelet analysis + synthesis round trip of the map.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+N > 1 runs under torchrun, one replica per rank (each rank transforms its own
+seeded map; "scaling": "weak"); timing is the max over ranks of CUDA-event time.
+--impl reference times the CPU oracle port of the same path (oracle/, C with
+OpenMP, the reference itself being pure Python that cannot leave this repo's
+build container) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "wavelet analysis+synthesis round-trips/s at L=2048; FP64 peak and HBM fraction"
+
+# BASELINE.json configs (SURVEY 8(d) spectra)
+CONFIGS = {
+    "C1": dict(L=64, batch=1, real=False, lam=2.0, j0=0, multires=False, spec="flat"),
+    "C2": dict(L=256, batch=16, real=True, lam=2.0, j0=2, multires=True, spec="cl"),
+    "C3": dict(L=1024, batch=8, real=False, lam=2.0, j0=3, multires=True, spec="flat"),
+    "C4": dict(L=2048, batch=1, real=False, lam=3.0, j0=2, multires=True, spec="l1"),
+    "C5": dict(L=4096, batch=1, real=True, lam=2.0, j0=0, multires=True, spec="beam"),
+}
+
+
+def spectrum(name, L):
+    ell = np.arange(L, dtype=np.float64)
+    if name == "flat":
+        return np.ones(L)
+    if name == "l1":
+        return (ell + 1.0) ** -2
+    base = np.where(ell >= 2, 1.0 / np.maximum(ell * (ell + 1.0), 1.0), 0.0)
+    if name == "cl":
+        return base
+    sigma = 5.0 / 60.0 * np.pi / 180.0
+    return base * np.exp(-ell * (ell + 1.0) * sigma**2 / 2.0)
+
+
+def seeded_coeffs(L, real, spec, seed):
+    from paper_1211_1680_b200 import gaussian_coeffs
+
+    f = gaussian_coeffs(L, np.random.default_rng(seed), real_signal=real)
+    ell = np.repeat(np.arange(L), 2 * np.arange(L) + 1)
+    return f.coeffs * np.sqrt(spectrum(spec, L))[ell]
+
+
+def legendre_flops(k, nsets, real):
+    """Canonical FLOPs of one Legendre stage: 4 B k S + 4 k k(k+1)/2."""
+    S = k * (k + 1) / 2 if real else k * k
+    return 4.0 * nsets * k * S + 4.0 * k * k * (k + 1) / 2
+
+
+def stage_flops(cfg, bands):
+    """Canonical FLOPs per launch of the two grouped Legendre launches of each direction."""
+    L, B, real = cfg["L"], cfg["batch"], cfg["real"]
+    groups = {}
+    for k in bands:
+        groups[k] = groups.get(k, 0) + B
+    grouped = sum(legendre_flops(k, n, real) for k, n in groups.items())
+    top = legendre_flops(L, B, real)
+    # analysis direction: leg_ana = top, leg_synth = grouped; synthesis: the mirror
+    return {"leg_ana": (top + grouped) / 2.0, "leg_synth": (top + grouped) / 2.0,
+            "per_rt": 2.0 * (top + grouped)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu, self.rows, self._stop = gpu_index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_ours(args, cfgname):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1211_1680_b200 as sw
+    from paper_1211_1680_b200 import _native
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg = CONFIGS[cfgname]
+    L, B, real = cfg["L"], cfg["batch"], cfg["real"]
+    scheme = sw.SamplingScheme.MW
+    tcfg = sw.TransformConfig(L, cfg["lam"], cfg["j0"], scheme=scheme, multires=cfg["multires"])
+    wt = WaveletTransform(tcfg, batch=B, real=real)
+
+    # seeded input (untimed setup): f_lm -> MW map through our own synthesis
+    flm = np.stack([seeded_coeffs(L, real, cfg["spec"], 1000 + 97 * rank + b) for b in range(B)])
+    sht = SphericalHarmonicTransform(scheme, L)
+    x = sht.synthesis(torch.from_numpy(flm).cuda(), real=real)
+    scale = wt.alloc_scale_maps()
+    out = torch.empty_like(x)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        wt.round_trip(x, scale, out)
+    torch.cuda.synchronize()
+    err = (out - x).abs().max().item() / x.abs().max().item()
+
+    # --- device-resident timed region
+    _native.profile_enable(True)
+    _native.profile_read(reset=True)
+    l0 = _native.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(st)
+        for _ in range(args.steps):
+            wt.round_trip(x, scale, out)
+        ev1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+    launches = _native.kernel_launches() - l0
+    prof = _native.profile_read(reset=True)
+    _native.profile_enable(False)
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    value = ws * B * args.steps / (ms / 1e3)
+
+    # --- end to end through the public API with pinned host buffers
+    x_host = x.cpu().pin_memory()
+    out_host = torch.empty_like(x_host).pin_memory()
+    for _ in range(max(1, args.warmup // 2)):
+        out_host.copy_(wt.round_trip(x_host, scale, out), non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        out_host.copy_(wt.round_trip(x_host, scale, out), non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = t.item()
+    e2e = ws * B * args.steps / (ms_e2e / 1e3)
+    nbytes = x.numel() * x.element_size()
+
+    fp64_peak = _native.fp64_peak_tflops(None)
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return None
+    fl = stage_flops(cfg, wt.bands)
+    dom = max(("leg_synth", "leg_ana"), key=lambda s: prof[s][0])
+    dms, dn = prof[dom]
+    achieved = fl[dom] / (dms / dn * 1e-3) / 1e12 if dn else None
+    stages = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+              for k, v in prof.items()}
+    rec = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "round-trips/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded Gaussian f_lm, BASELINE spectrum; MW map from our synthesis)",
+        "config": {
+            "workload": f"{cfgname}: L={L} MW {'real' if real else 'complex'} x{B}, "
+                        f"lambda={cfg['lam']:g}, J0={cfg['j0']}, "
+                        f"{'multires' if cfg['multires'] else 'full-res'}",
+            "L": L, "batch": B, "bands": list(wt.bands),
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+            "l2": f"inputs larger than L2 (map {nbytes / 1e6:.0f} MB, working set > 1 GB)",
+        },
+        "e2e": {"value": e2e, "unit": "round-trips/s", "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes},
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "fp64", "kernel": dom,
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak if achieved else None,
+            "traffic": None,
+            "flops_per_launch": fl[dom],
+            "peak_source": "measured DFMA microbenchmark (s2w_fp64_peak) in this run; "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+        },
+        "stages": stages,
+        "canonical_flops_per_rt": fl["per_rt"],
+        "fp64_tflops_per_rt": fl["per_rt"] * value / ws / 1e12,
+        "rt_rel_err": err,
+        "clocks": clk.summary(),
+    }
+    rec["cpu_baseline"] = cpu_baseline(cfgname, args) if not args.no_cpu else None
+    if ws > 1:
+        dist.destroy_process_group()
+    return rec
+
+
+def cpu_baseline(cfgname, args):
+    try:
+        from oracle import oracle as orc
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "round-trips/s", "error": f"oracle unavailable: {e}"}
+    return orc.bench_sample(CONFIGS[cfgname], seconds=args.cpu_seconds)
+
+
+def run_reference(args, cfgname):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    from oracle import oracle as orc
+
+    cfg = CONFIGS[cfgname]
+    steps = []
+    for _ in range(args.warmup):
+        orc.bench_sample(cfg, seconds=args.cpu_seconds)
+    for _ in range(args.steps):
+        steps.append(orc.bench_sample(cfg, seconds=args.cpu_seconds))
+    vals = [s["value"] for s in steps]
+    v = float(np.mean(vals))
+    s0 = steps[0]
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "round-trips/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / v if v else None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgname, "L": cfg["L"], "batch": cfg["batch"]},
+        "cpu_baseline": {"value": v, "unit": "round-trips/s", "cores": s0["cores"],
+                         "kind": s0["kind"], "sample": s0["sample"]},
+        "e2e": {"value": v, "unit": "round-trips/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rec = run_reference(args, args.config) if args.impl == "reference" else run_ours(args, args.config)
+    if rec is not None:
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,18 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* plan, const double* const* scale_maps,
  * s2w_wav_synthesis_pixel the recombined f_lm (transform.py:196-200). */
 int s2w_wav_plan_flm(s2w_wav_plan* plan, double** flm);
 
+/* ---------------------------------------------------------------- accounting */
+/* Number of kernels launched by this library since load (bench "gpu_launches"). */
+long long s2w_kernel_launches(void);
+/* Per-stage CUDA-event timing of every launch (off by default). */
+int s2w_profile_enable(int on);
+/* ms[i], count[i] for stage i < n in the order of s2w_profile_stage_name(i);
+ * synchronises on the recorded events; reset != 0 clears the accumulators. */
+int s2w_profile_read(int n, double* ms, long long* count, int reset);
+const char* s2w_profile_stage_name(int i);
+/* Measured FP64 FMA throughput of the current device in TFLOP/s (synchronous). */
+int s2w_fp64_peak(double* tflops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

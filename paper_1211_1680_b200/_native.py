@@ -40,6 +40,12 @@ _PROTOS = {
     "s2w_wav_synthesis_harmonic": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_wav_analysis_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "s2w_wav_synthesis_pixel": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_kernel_launches": (ctypes.c_longlong, []),
+    "s2w_profile_enable": (_c_int, [_c_int]),
+    "s2w_profile_read": (
+        _c_int, [_c_int, _dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
+    "s2w_profile_stage_name": (ctypes.c_char_p, [_c_int]),
+    "s2w_fp64_peak": (_c_int, [_dp, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_PROTOS)
@@ -82,3 +88,29 @@ def check(status: int) -> None:
 
 def version() -> str:
     return load().s2w_version().decode()
+
+
+N_STAGES = 6
+
+
+def kernel_launches() -> int:
+    return int(load().s2w_kernel_launches())
+
+
+def profile_enable(on: bool) -> None:
+    check(load().s2w_profile_enable(int(bool(on))))
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{stage: (milliseconds, launches)} accumulated since the last reset."""
+    lib = load()
+    ms = (ctypes.c_double * N_STAGES)()
+    cnt = (ctypes.c_longlong * N_STAGES)()
+    check(lib.s2w_profile_read(N_STAGES, ms, cnt, int(reset)))
+    return {lib.s2w_profile_stage_name(i).decode(): (ms[i], int(cnt[i])) for i in range(N_STAGES)}
+
+
+def fp64_peak_tflops(stream=None) -> float:
+    v = ctypes.c_double()
+    check(load().s2w_fp64_peak(ctypes.byref(v), stream))
+    return v.value

@@ -96,6 +96,57 @@ struct DevBuf {
   }
 };
 
+// ------------------------------------------------------------------ launch accounting
+// Every kernel launch made by the library bumps g_launches (reported by
+// bench.py as "gpu_launches").  With profiling enabled, each launch is also
+// bracketed by CUDA events on its stream and accumulated per stage.
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+
+enum ProfStage { P_LEG_SYNTH = 0, P_LEG_ANA, P_PHI_FWD, P_THETA, P_PHI_INV, P_TILE, P_NSTAGE };
+static const char* kStageNames[P_NSTAGE] = {"leg_synth", "leg_ana", "phi_fwd",
+                                            "theta", "phi_inv", "tile"};
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_pending;
+static std::vector<cudaEvent_t> g_prof_pool;
+static double g_prof_ms[P_NSTAGE] = {0};
+static long long g_prof_n[P_NSTAGE] = {0};
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int s, cudaStream_t stream) : stage(s), st(stream) {
+    ++g_launches;
+    if (g_prof) {
+      a = prof_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, st);
+      g_prof_pending.push_back({stage, a, b});
+    }
+  }
+};
+
 // ------------------------------------------------------------------ grids (host)
 typedef long double ld;
 static const ld PI_L = 3.141592653589793238462643383279502884L;
@@ -527,6 +578,7 @@ static int run_synth(const SynthCfg& cfg, const double* seed_c, double2* const* 
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
+  ProfScope ps(P_LEG_SYNTH, st);
   CU(launch_leg_synth(a, st));
   return S2W_OK;
 }
@@ -543,6 +595,7 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
+  ProfScope ps(P_LEG_ANA, st);
   CU(launch_leg_ana(a, st));
   return S2W_OK;
 }
@@ -560,7 +613,10 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
   pa.out = G;
   pa.n_bins = g->n_bins(!real);
   pa.scale = 1.0 / (double)g->N;
-  CU(launch_phi_fwd(pa, st));
+  {
+    ProfScope ps(P_PHI_FWD, st);
+    CU(launch_phi_fwd(pa, st));
+  }
   if (g->scheme == S2W_SCHEME_MW) {
     ThetaArgs ta;
     ta.T = g->fft();
@@ -569,6 +625,7 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
     ta.n_bins = g->n_bins(!real);
     ta.in = G;
     ta.out = G;
+    ProfScope ps(P_THETA, st);
     CU(launch_theta(ta, st));
   }
   return S2W_OK;
@@ -586,6 +643,7 @@ static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2*
   pa.in = G;
   pa.out = map;
   pa.n_bins = g->n_bins(!real);
+  ProfScope ps(P_PHI_INV, st);
   CU(launch_phi_inv(pa, st));
   return S2W_OK;
 }
@@ -908,6 +966,7 @@ int s2w_wav_analysis_harmonic(s2w_wav_plan* p, int truncate, const double* flm,
   }
   a.f_in = (const double2*)flm;
   a.f_out = nullptr;
+  ProfScope ps(P_TILE, (cudaStream_t)stream);
   CU(launch_tile_analysis(a, (cudaStream_t)stream));
   return S2W_OK;
 }
@@ -928,6 +987,7 @@ int s2w_wav_synthesis_harmonic(s2w_wav_plan* p, int full_band, const double* con
   }
   a.f_in = nullptr;
   a.f_out = (double2*)flm;
+  ProfScope ps(P_TILE, (cudaStream_t)stream);
   CU(launch_tile_synthesis(a, (cudaStream_t)stream));
   return S2W_OK;
 }
@@ -972,6 +1032,51 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, do
   // sh_synthesis at L (transform.py:200)
   CHECK(run_synth(p->syn_top, p->top->seed_c, bufs, st));
   CHECK(inverse_rings(p->top, p->B, !cplx, p->Gtop.as<double2>(), map, st));
+  return S2W_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ accounting / probes
+extern "C" {
+
+long long s2w_kernel_launches(void) { return g_launches.load(); }
+
+int s2w_profile_enable(int on) {
+  g_prof = on != 0;
+  return S2W_OK;
+}
+
+// Synchronises on the recorded events, accumulates per-stage milliseconds and
+// launch counts since the last reset, and writes them in stage order
+// (leg_synth, leg_ana, phi_fwd, theta, phi_inv, tile).  n = capacity.
+int s2w_profile_read(int n, double* ms, long long* count, int reset) {
+  for (auto& r : g_prof_pending) {
+    float t = 0.f;
+    CU(cudaEventSynchronize(r.b));
+    CU(cudaEventElapsedTime(&t, r.a, r.b));
+    g_prof_ms[r.stage] += t;
+    g_prof_n[r.stage] += 1;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_pending.clear();
+  for (int i = 0; i < n && i < P_NSTAGE; ++i) {
+    if (ms) ms[i] = g_prof_ms[i];
+    if (count) count[i] = g_prof_n[i];
+  }
+  if (reset)
+    for (int i = 0; i < P_NSTAGE; ++i) {
+      g_prof_ms[i] = 0;
+      g_prof_n[i] = 0;
+    }
+  return S2W_OK;
+}
+
+const char* s2w_profile_stage_name(int i) { return (i >= 0 && i < P_NSTAGE) ? kStageNames[i] : ""; }
+
+int s2w_fp64_peak(double* tflops, void* stream) {
+  CU(s2w::measure_fp64_peak(tflops, (cudaStream_t)stream));
   return S2W_OK;
 }
 

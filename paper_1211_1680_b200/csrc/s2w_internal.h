@@ -144,4 +144,8 @@ cudaError_t launch_tile_analysis(const TileArgs& a, cudaStream_t st);
 // f[set][i] = sum_j fac_j[l] * in_j[set][i] (i < band_j^2), j ascending (transform.py:153-172)
 cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st);
 
+// FP64 FMA throughput microbenchmark (roofline denominator for the Legendre
+// stage; MEASURED_PEAKS.json has no FP64 entry).  Synchronises the stream.
+cudaError_t measure_fp64_peak(double* tflops, cudaStream_t st);
+
 }  // namespace s2w

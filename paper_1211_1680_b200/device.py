@@ -1,0 +1,123 @@
+"""Device-resident public API (torch tensors in, torch tensors out).
+
+The numpy drop-in (``sht``/``transform``) copies host arrays in and out on every
+call.  These classes keep maps and coefficients in HBM and expose the same
+transforms on torch tensors; host tensors (ideally pinned) are copied to the
+device inside the call, which is what bench.py's end-to-end figure times.
+
+Layouts: complex maps are complex128 tensors (batch, L, 2L-1); real maps are
+float64 tensors of the same shape; coefficients are complex128 (batch, L*L).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device, _native
+from .errors import ParameterError
+from .grid import make_grid, scheme_code
+from .transform import TransformConfig, kernels_for, scale_bands
+
+__all__ = ["WaveletTransform", "SphericalHarmonicTransform"]
+
+
+def _on_device(t):
+    if t.is_cuda:
+        return t.contiguous()
+    return t.to(device=f"cuda:{_device.device_index()}", non_blocking=True)
+
+
+class SphericalHarmonicTransform:
+    """SHT on one grid for batches of device tensors."""
+
+    def __init__(self, scheme, L: int):
+        _device.require_cuda()
+        self.grid = make_grid(scheme, L)
+        self.plan = _device.sht_plan(scheme_code(scheme), L)
+
+    def synthesis(self, flm, real: bool = False):
+        th = _device.torch()
+        flm = _on_device(flm)
+        n = flm.shape[0]
+        Lc = int(round(np.sqrt(flm.shape[1])))
+        g = self.grid
+        dt = th.float64 if real else th.complex128
+        out = th.empty((n, g.n_theta, g.n_phi), dtype=dt, device=flm.device)
+        _native.check(_native.load().s2w_sh_synthesis(
+            self.plan.handle, n, Lc, int(real), _device.ptr(flm), _device.ptr(out),
+            _device.stream_handle()))
+        return out
+
+    def analysis(self, maps):
+        th = _device.torch()
+        maps = _on_device(maps)
+        real = not maps.is_complex()
+        n = maps.shape[0]
+        L = self.grid.L
+        out = th.empty((n, L * L), dtype=th.complex128, device=maps.device)
+        _native.check(_native.load().s2w_sh_analysis(
+            self.plan.handle, n, int(real), _device.ptr(maps), _device.ptr(out),
+            _device.stream_handle()))
+        return out
+
+
+class WaveletTransform:
+    """Wavelet analysis/synthesis of ``batch`` maps sharing one TransformConfig."""
+
+    def __init__(self, config: TransformConfig, batch: int = 1, real: bool = False):
+        _device.require_cuda()
+        if batch < 1:
+            raise ParameterError("batch must be >= 1")
+        self.config, self.batch, self.real = config, batch, bool(real)
+        kern = kernels_for(config)
+        self.bands = scale_bands(config, kern)
+        self.plan = _device.wav_plan(scheme_code(config.scheme), config.L, batch, real,
+                                     kern.table(), self.bands)
+        self.grids = [make_grid(config.scheme, k) for k in self.bands]
+        self.map_shape = (batch, config.L, 2 * config.L - 1)
+
+    def _dtype(self):
+        th = _device.torch()
+        return th.float64 if self.real else th.complex128
+
+    def alloc_scale_maps(self):
+        th = _device.torch()
+        return [th.empty((self.batch, g.n_theta, g.n_phi), dtype=self._dtype(),
+                         device=f"cuda:{_device.device_index()}") for g in self.grids]
+
+    def analysis(self, x, outs=None):
+        """x: (batch, L, 2L-1) map tensor -> [scaling, j0..J] map tensors."""
+        x = _on_device(x)
+        if tuple(x.shape) != self.map_shape or x.dtype != self._dtype():
+            raise ParameterError(f"expected {self._dtype()} tensor of shape {self.map_shape}")
+        outs = self.alloc_scale_maps() if outs is None else outs
+        _native.check(_native.load().s2w_wav_analysis_pixel(
+            self.plan.handle, _device.ptr(x), _device.ptr_array(outs), _device.stream_handle()))
+        return outs
+
+    def synthesis(self, maps, out=None):
+        th = _device.torch()
+        maps = [_on_device(m) for m in maps]
+        if out is None:
+            out = th.empty(self.map_shape, dtype=self._dtype(), device=maps[0].device)
+        _native.check(_native.load().s2w_wav_synthesis_pixel(
+            self.plan.handle, _device.ptr_array(maps), _device.ptr(out), _device.stream_handle()))
+        return out
+
+    def round_trip(self, x, scale_maps=None, out=None):
+        return self.synthesis(self.analysis(x, scale_maps), out)
+
+    def flm(self):
+        """View of the plan's f_lm workspace (batch, L*L) complex128."""
+        import ctypes
+
+        th = _device.torch()
+        p = ctypes.c_void_p()
+        _native.check(_native.load().s2w_wav_plan_flm(self.plan.handle, ctypes.byref(p)))
+        L = self.config.L
+        # wrap the device pointer through __cuda_array_interface__
+        class _Wrap:
+            __cuda_array_interface__ = {
+                "shape": (self.batch, L * L, 2), "typestr": "<f8", "data": (p.value, False),
+                "version": 3, "strides": None,
+            }
+        return th.view_as_complex(th.as_tensor(_Wrap(), device=f"cuda:{_device.device_index()}"))
