@@ -131,6 +131,8 @@ int s2w_profile_read(int n, double* ms, long long* count, int reset);
 const char* s2w_profile_stage_name(int i);
 /* Measured FP64 FMA throughput of the current device in TFLOP/s (synchronous). */
 int s2w_fp64_peak(double* tflops, void* stream);
+/* Measured FP64 tensor-core (DMMA m8n8k4) throughput in TFLOP/s (synchronous). */
+int s2w_dmma_peak(double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,7 @@ _PROTOS = {
         _c_int, [_c_int, _dp, ctypes.POINTER(ctypes.c_longlong), _c_int]),
     "s2w_profile_stage_name": (ctypes.c_char_p, [_c_int]),
     "s2w_fp64_peak": (_c_int, [_dp, _vp]),
+    "s2w_dmma_peak": (_c_int, [_dp, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_PROTOS)
@@ -113,4 +114,10 @@ def profile_read(reset: bool = True) -> dict:
 def fp64_peak_tflops(stream=None) -> float:
     v = ctypes.c_double()
     check(load().s2w_fp64_peak(ctypes.byref(v), stream))
+    return v.value
+
+
+def dmma_peak_tflops(stream=None) -> float:
+    v = ctypes.c_double()
+    check(load().s2w_dmma_peak(ctypes.byref(v), stream))
     return v.value

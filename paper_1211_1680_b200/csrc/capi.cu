@@ -443,14 +443,14 @@ struct SynthCfg {
   bool built = false;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, items;
-  int n_items = 0, ns = 1, cplx = 1;
+  int n_items = 0, ns = 1, cplx = 1, win = 32;
 };
 
 struct AnaCfg {
   bool built = false;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, segs, items;
-  int n_items = 0, ns = 1, cplx = 1;
+  int n_items = 0, ns = 1, cplx = 1, win = 32;
 };
 
 // A synthesis "group": sets sharing one grid.
@@ -493,6 +493,9 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   cfg.n_items = (int)its.size();
   cfg.ns = ns;
   cfg.cplx = cplx;
+  int kmax = 1;
+  for (auto& gr : groups) kmax = std::max(kmax, gr.g->k);
+  cfg.win = leg_synth_window(kmax, ns, cplx);
   cfg.built = true;
   return S2W_OK;
 }
@@ -563,6 +566,7 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   cfg.n_items = (int)its.size();
   cfg.ns = ns;
   cfg.cplx = cplx;
+  cfg.win = leg_ana_window(kmax, ns, cplx);
   cfg.built = true;
   return S2W_OK;
 }
@@ -577,6 +581,7 @@ static int run_synth(const SynthCfg& cfg, const double* seed_c, double2* const* 
   a.n_items = cfg.n_items;
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
+  a.win = cfg.win;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_SYNTH, st);
   CU(launch_leg_synth(a, st));
@@ -594,6 +599,7 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
   a.n_items = cfg.n_items;
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
+  a.win = cfg.win;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_ANA, st);
   CU(launch_leg_ana(a, st));
@@ -1077,6 +1083,11 @@ const char* s2w_profile_stage_name(int i) { return (i >= 0 && i < P_NSTAGE) ? kS
 
 int s2w_fp64_peak(double* tflops, void* stream) {
   CU(s2w::measure_fp64_peak(tflops, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+int s2w_dmma_peak(double* tflops, void* stream) {
+  CU(s2w::measure_dmma_peak(tflops, (cudaStream_t)stream));
   return S2W_OK;
 }
 

@@ -104,6 +104,7 @@ struct LegSynthArgs {
   int n_items;
   int cplx;
   int ns;  // compile-time set width selected by the launcher
+  int win; // degrees per shared-memory window (leg_synth_window)
   double2* bufs[S2W_NBUF];
 };
 
@@ -116,11 +117,14 @@ struct LegAnaArgs {
   int n_items;
   int cplx;
   int ns;
+  int win;  // degrees per window (leg_ana_window)
   double2* bufs[S2W_NBUF];
 };
 
 cudaError_t launch_leg_synth(const LegSynthArgs& a, cudaStream_t st);
 cudaError_t launch_leg_ana(const LegAnaArgs& a, cudaStream_t st);
+int leg_synth_window(int kmax, int ns, int cplx);
+int leg_ana_window(int kmax, int ns, int cplx);
 // Per ring: largest order m whose Legendre column reaches the significance
 // threshold below degree k (used to build the per-m active ring ranges).
 cudaError_t launch_leg_probe(int k, int n_t, const double* cos_t, const double* sin_t,
@@ -147,5 +151,7 @@ cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st);
 // FP64 FMA throughput microbenchmark (roofline denominator for the Legendre
 // stage; MEASURED_PEAKS.json has no FP64 entry).  Synchronises the stream.
 cudaError_t measure_fp64_peak(double* tflops, cudaStream_t st);
+// FP64 tensor-core (mma.sync m8n8k4 DMMA) throughput in TFLOP/s.
+cudaError_t measure_dmma_peak(double* tflops, cudaStream_t st);
 
 }  // namespace s2w
