@@ -51,6 +51,12 @@ _PROTOS = {
 
 EXPORTED_SYMBOLS = tuple(_PROTOS)
 
+# stage hooks (include/s2w_testing.h), bound lazily by tests
+_TEST_PROTOS = {
+    "s2w_test_rings_inverse": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "s2w_test_rings_forward": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+}
+
 _lib = None
 
 
@@ -69,7 +75,7 @@ def load() -> ctypes.CDLL:
             "`python -c 'import __graft_entry__ as g; g.build()'` (or `make`)"
         )
     lib = ctypes.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
-    for name, (res, args) in _PROTOS.items():
+    for name, (res, args) in {**_PROTOS, **_TEST_PROTOS}.items():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

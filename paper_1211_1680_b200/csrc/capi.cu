@@ -289,7 +289,7 @@ struct GridRes {
   std::vector<int2> act_host;
   double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
   int2* act = nullptr;
-  double2 *tw = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
+  double2 *oct = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
   double* seed_c = nullptr;
 
@@ -297,7 +297,7 @@ struct GridRes {
     FftTablesDev t;
     t.N = N;
     t.logM = logM;
-    t.tw = tw;
+    t.oct = oct;
     t.chirp = chirp;
     t.bl_fwd = bl_fwd;
     t.bl_inv = bl_inv;
@@ -388,10 +388,10 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->act, g->act_host));
 
   // FFT / Bluestein / theta-stage tables
-  std::vector<double2> tw(M), chirp(N), ph1(N), ph2(N);
-  for (int j = 0; j < M; ++j) {
-    ld ang = -2.0L * PI_L * (ld)j / (ld)M;
-    tw[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
+  std::vector<double2> oct(M / 8 + 1), chirp(N), ph1(N), ph2(N);
+  for (int j = 0; j <= M / 8; ++j) {
+    ld ang = 2.0L * PI_L * (ld)j / (ld)M;
+    oct[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
   }
   std::vector<cld> cl(N);
   for (int n = 0; n < N; ++n) {
@@ -419,7 +419,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     ph1[bin] = d2(cl[bin] * cld(std::cos(a1), std::sin(a1)) / (ld)N);
     ph2[bin] = d2(cld(std::cos(-a1), std::sin(-a1)) * std::conj(cl[bin]));
   }
-  CHECK(upload_new(&g->tw, tw));
+  CHECK(upload_new(&g->oct, oct));
   CHECK(upload_new(&g->chirp, chirp));
   CHECK(upload_new(&g->bl_fwd, spectrum_brev(b)));
   CHECK(upload_new(&g->bl_inv, spectrum_brev(cc)));
@@ -1088,6 +1088,55 @@ int s2w_fp64_peak(double* tflops, void* stream) {
 
 int s2w_dmma_peak(double* tflops, void* stream) {
   CU(s2w::measure_dmma_peak(tflops, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ stage hooks (tests)
+// Individual pipeline stages on one grid, for stage-level parity tests
+// (include/s2w_testing.h).  Same kernels as the transforms above.
+extern "C" {
+
+int s2w_test_rings_inverse(int scheme, int L, int n_sets, int is_real, const double* G,
+                           double* map, void* stream) {
+  int dev;
+  CU(cudaGetDevice(&dev));
+  GridRes* g;
+  CHECK(get_grid(dev, scheme, L, &g));
+  return inverse_rings(g, n_sets, is_real != 0, (const double2*)G, map, (cudaStream_t)stream);
+}
+
+int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta_stage,
+                           const double* map, double* G, void* stream) {
+  int dev;
+  CU(cudaGetDevice(&dev));
+  GridRes* g;
+  CHECK(get_grid(dev, scheme, L, &g));
+  PhiFwdArgs pa;
+  pa.T = g->fft();
+  pa.n_sets = n_sets;
+  pa.n_rings = g->k;
+  pa.real = is_real ? 1 : 0;
+  pa.in = map;
+  pa.out = (double2*)G;
+  pa.n_bins = g->n_bins(!is_real);
+  pa.scale = 1.0 / (double)g->N;
+  {
+    ProfScope ps(P_PHI_FWD, (cudaStream_t)stream);
+    CU(launch_phi_fwd(pa, (cudaStream_t)stream));
+  }
+  if (theta_stage) {
+    ThetaArgs ta;
+    ta.T = g->fft();
+    ta.n_sets = n_sets;
+    ta.k = g->k;
+    ta.n_bins = g->n_bins(!is_real);
+    ta.in = (double2*)G;
+    ta.out = (double2*)G;
+    ProfScope ps(P_THETA, (cudaStream_t)stream);
+    CU(launch_theta(ta, (cudaStream_t)stream));
+  }
   return S2W_OK;
 }
 

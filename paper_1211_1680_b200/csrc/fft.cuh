@@ -124,11 +124,45 @@ template <> S2W_DEV void bfly_inv<8>(double2* v) {
   v[7] = csub(b3, t);
 }
 
+// W_M^k = exp(-2 pi i k / M) from an octant table oct[r] = (cos, sin)(2 pi r / M),
+// r in [0, M/8], held in shared memory (M/8 + 1 entries: 16 KiB at M = 8192).
+S2W_DEV double2 twiddle(int k, const double2* __restrict__ oct, int logM) {
+  const int sh = logM - 3;
+  const int M8 = 1 << sh;
+  const int q = (k >> sh) & 7;
+  int r = k & (M8 - 1);
+  if (q & 1) r = M8 - r;
+  const double2 e = oct[r];
+  const bool swap = ((q + 1) & 2) != 0;          // q in {1, 2, 5, 6}
+  double c = swap ? e.y : e.x;
+  double s = swap ? e.x : e.y;
+  if (q >= 2 && q <= 5) c = -c;                  // cos(phi) < 0
+  if (q >= 4) s = -s;                            // sin(phi) < 0
+  return make_double2(c, -s);
+}
+
+// Twiddles of one radix-R butterfly: w[r] = u^r, u = W_M^ts (one table lookup,
+// then products; at most 3 roundings deep for R = 8).
+template <int R>
+S2W_DEV void twiddle_powers(double2* w, int ts, const double2* __restrict__ oct, int logM) {
+  const double2 u = twiddle(ts, oct, logM);
+  w[1] = u;
+  if (R >= 4) {
+    w[2] = cmul(u, u);
+    w[3] = cmul(w[2], u);
+  }
+  if (R >= 8) {
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], u);
+    w[6] = cmul(w[3], w[3]);
+    w[7] = cmul(w[4], w[3]);
+  }
+}
+
 // One radix-R pass of span s = 2^log2s over a row of M elements.
-// tw[k] = exp(-2 pi i k / M), k < M.
 template <int R, bool INV>
 S2W_DEV void fft_pass(double2* __restrict__ buf, int logM, int log2s,
-                      const double2* __restrict__ tw, int gtid, int gsize) {
+                      const double2* __restrict__ oct, int gtid, int gsize) {
   const int M = 1 << logM;
   const int s = 1 << log2s;
   const int nb = M / R;
@@ -139,17 +173,20 @@ S2W_DEV void fft_pass(double2* __restrict__ buf, int logM, int log2s,
     double2 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = buf[swz(base + i * s)];
-    const int ts = j * tstep;
     if (!INV) {
       bfly_fwd<R>(v);
       if (j) {
+        double2 w[R];
+        twiddle_powers<R>(w, j * tstep, oct, logM);
 #pragma unroll
-        for (int i = 1; i < R; ++i) v[i] = cmul(v[i], __ldg(&tw[brev<R>(i) * ts]));
+        for (int i = 1; i < R; ++i) v[i] = cmul(v[i], w[brev<R>(i)]);
       }
     } else {
       if (j) {
+        double2 w[R];
+        twiddle_powers<R>(w, j * tstep, oct, logM);
 #pragma unroll
-        for (int i = 1; i < R; ++i) v[i] = cmulc(v[i], __ldg(&tw[brev<R>(i) * ts]));
+        for (int i = 1; i < R; ++i) v[i] = cmulc(v[i], w[brev<R>(i)]);
       }
       bfly_inv<R>(v);
     }
@@ -158,10 +195,17 @@ S2W_DEV void fft_pass(double2* __restrict__ buf, int logM, int log2s,
   }
 }
 
+// Copy the octant table (M/8 + 1 entries) from global into shared memory.
+S2W_DEV void load_octant(double2* __restrict__ s_oct, const double2* __restrict__ g_oct, int logM) {
+  const int n = (1 << (logM - 3)) + 1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_oct[i] = __ldg(&g_oct[i]);
+}
+
 // Forward DIF FFT: natural -> bit-reversed.  Ends with a __syncthreads.
 // Precondition: the row is fully written and visible (caller synced).
 S2W_DEV void fft_fwd(double2* buf, int logM, const double2* __restrict__ tw, int gtid,
                      int gsize) {
+  // tw: shared-memory octant table (load_octant)
   int ls = logM;
   while (ls >= 3) {
     ls -= 3;
@@ -199,7 +243,20 @@ S2W_DEV void fft_inv(double2* buf, int logM, const double2* __restrict__ tw, int
 }
 
 // buf[p] *= tab[p] for all p (tab stored in the same bit-reversed order).
+// Unrolled so that 8 table loads per thread are in flight at once.
 S2W_DEV void pointwise_mul(double2* buf, int M, const double2* __restrict__ tab, int gtid,
                            int gsize) {
-  for (int p = gtid; p < M; p += gsize) buf[swz(p)] = cmul(buf[swz(p)], __ldg(&tab[p]));
+  for (int p0 = gtid; p0 < M; p0 += 8 * gsize) {
+    double2 t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = p0 + u * gsize;
+      t[u] = (p < M) ? __ldg(&tab[p]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = p0 + u * gsize;
+      if (p < M) buf[swz(p)] = cmul(buf[swz(p)], t[u]);
+    }
+  }
 }

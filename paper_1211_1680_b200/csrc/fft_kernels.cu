@@ -32,6 +32,8 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
   const int M = 1 << T.logM, N = T.N;
   const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
   double2* buf = smem + (size_t)grp * M;
+  double2* oct = smem + (size_t)a.rpc * M;
+  load_octant(oct, T.oct, T.logM);
   const int row = blockIdx.x * a.rpc + grp;
   const int n_rows = a.n_sets * a.n_rings;
   const bool valid = row < n_rows;
@@ -39,21 +41,41 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
   const int t = valid ? row - set * a.n_rings : 0;
   const long long in_base = ((long long)set * a.n_rings + t) * N;
 
-  for (int n = gtid; n < M; n += a.gsize) {
-    double2 v = make_double2(0.0, 0.0);
-    if (valid && n < N) v = cmul(load_map_elem(a.in, in_base + n, a.real), __ldg(&T.chirp[n]));
-    buf[swz(n)] = v;
+  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+    double2 x[8], c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      const bool in = valid && n < N;
+      x[u] = in ? load_map_elem(a.in, in_base + n, a.real) : make_double2(0.0, 0.0);
+      c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
+    }
   }
   __syncthreads();
-  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
   pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
   __syncthreads();
-  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_inv(buf, T.logM, oct, gtid, a.gsize);
   if (!valid) return;
   double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
-  for (int mi = gtid; mi < a.n_bins; mi += a.gsize) {
-    double2 v = cscale(cmul(__ldg(&T.chirp[mi]), buf[swz(mi)]), a.scale);
-    out[(size_t)mi * a.n_rings + t] = v;
+  for (int m0 = gtid; m0 < a.n_bins; m0 += 8 * a.gsize) {
+    double2 c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int mi = m0 + u * a.gsize;
+      c[u] = (mi < a.n_bins) ? __ldg(&T.chirp[mi]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int mi = m0 + u * a.gsize;
+      if (mi < a.n_bins)
+        out[(size_t)mi * a.n_rings + t] = cscale(cmul(c[u], buf[swz(mi)]), a.scale);
+    }
   }
 }
 
@@ -64,6 +86,8 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   const int M = 1 << T.logM, N = T.N;
   const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
   double2* buf = smem + (size_t)grp * M;
+  double2* oct = smem + (size_t)a.rpc * M;
+  load_octant(oct, T.oct, T.logM);
   const int row = blockIdx.x * a.rpc + grp;
   const int n_rows = a.n_sets * a.n_rings;
   const bool valid = row < n_rows;
@@ -71,39 +95,56 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   const int t = valid ? row - set * a.n_rings : 0;
   const double2* G = a.in + ((size_t)set * a.n_rings + t) * a.n_bins;
 
-  for (int n = gtid; n < M; n += a.gsize) {
-    double2 v = make_double2(0.0, 0.0);
-    if (valid && n < N) {
-      if (!a.real) {
-        v = __ldg(&G[n]);
-      } else if (n < a.n_bins) {
-        v = __ldg(&G[n]);
-        if (n == 0) v.y = 0.0;  // irfft ignores Im of the DC bin
-      } else {
-        v = cconj(__ldg(&G[N - n]));
+  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+    double2 x[8], c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      x[u] = make_double2(0.0, 0.0);
+      c[u] = make_double2(0.0, 0.0);
+      if (valid && n < N) {
+        if (!a.real) {
+          x[u] = __ldg(&G[n]);
+        } else if (n < a.n_bins) {
+          x[u] = __ldg(&G[n]);
+          if (n == 0) x[u].y = 0.0;  // irfft ignores Im of the DC bin
+        } else {
+          x[u] = cconj(__ldg(&G[N - n]));
+        }
+        c[u] = __ldg(&T.chirp[n]);
       }
-      v = cmulc(v, __ldg(&T.chirp[n]));
     }
-    buf[swz(n)] = v;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      if (n < M) buf[swz(n)] = cmulc(x[u], c[u]);
+    }
   }
   __syncthreads();
-  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
   pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
   __syncthreads();
-  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_inv(buf, T.logM, oct, gtid, a.gsize);
   if (!valid) return;
   const bool pole = a.mw_pole && t == a.n_rings - 1;
   double2 pv = make_double2(0.0, 0.0);
   if (pole) pv = __ldg(&G[0]);
   const size_t ob = ((size_t)set * a.n_rings + t) * N;
-  if (a.real) {
-    double* out = a.out + ob;
-    for (int p = gtid; p < N; p += a.gsize)
-      out[p] = pole ? pv.x : cmulc(buf[swz(p)], __ldg(&T.chirp[p])).x;
-  } else {
-    double2* out = reinterpret_cast<double2*>(a.out) + ob;
-    for (int p = gtid; p < N; p += a.gsize)
-      out[p] = pole ? pv : cmulc(buf[swz(p)], __ldg(&T.chirp[p]));
+  for (int p0 = gtid; p0 < N; p0 += 8 * a.gsize) {
+    double2 c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = p0 + u * a.gsize;
+      c[u] = (p < N) ? __ldg(&T.chirp[p]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = p0 + u * a.gsize;
+      if (p >= N) continue;
+      const double2 v = pole ? pv : cmulc(buf[swz(p)], c[u]);
+      if (a.real) a.out[ob + p] = v.x;
+      else reinterpret_cast<double2*>(a.out)[ob + p] = v;
+    }
   }
 }
 
@@ -114,6 +155,8 @@ __global__ void theta_kernel(ThetaArgs a) {
   const int M = 1 << T.logM, N = T.N, k = a.k;
   const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
   double2* buf = smem + (size_t)grp * M;
+  double2* oct = smem + (size_t)a.rpc * M;
+  load_octant(oct, T.oct, T.logM);
   const int row = blockIdx.x * a.rpc + grp;
   const int n_rows = a.n_sets * a.n_bins;
   const bool valid = row < n_rows;
@@ -124,52 +167,93 @@ __global__ void theta_kernel(ThetaArgs a) {
   const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
 
   // 1. parity extension to the full circle, times the Bluestein chirp
-  for (int n = gtid; n < M; n += a.gsize) {
-    double2 v = make_double2(0.0, 0.0);
-    if (valid && n < N) {
-      v = (n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn);
-      v = cmul(v, __ldg(&T.chirp[n]));
+  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+    double2 x[8], c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      const bool in = valid && n < N;
+      x[u] = in ? ((n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn))
+                : make_double2(0.0, 0.0);
+      c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
     }
-    buf[swz(n)] = v;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * a.gsize;
+      if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
+    }
   }
   __syncthreads();
   // 2. DFT_N (Bluestein)
-  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
   pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
   __syncthreads();
-  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_inv(buf, T.logM, oct, gtid, a.gsize);
   // 3. Fourier coefficients a_{m'} = c_bin e^{-i pi m'/N} conv[bin] / N, laid out
   //    over the length-M circle (negative m' at the top)
-  for (int bin = gtid; bin < N; bin += a.gsize) {
-    double2 v = cmul(buf[swz(bin)], __ldg(&T.ph1[bin]));
-    if (bin < k) buf[swz(bin)] = v;
-    else buf[swz(M - N + bin)] = v;
+  for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
+    double2 ph[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = b0 + u * a.gsize;
+      ph[u] = (bin < N) ? __ldg(&T.ph1[bin]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = b0 + u * a.gsize;
+      if (bin >= N) continue;
+      const double2 v = cmul(buf[swz(bin)], ph[u]);
+      buf[swz(bin < k ? bin : M - N + bin)] = v;
+    }
   }
   __syncthreads();
   for (int n = k + gtid; n < M - k + 1; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 4. convolution with the |sin theta| series (precomputed spectrum)
-  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
   pointwise_mul(buf, M, T.wconv, gtid, a.gsize);
   __syncthreads();
-  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_inv(buf, T.logM, oct, gtid, a.gsize);
   // 5. back onto N bins with the e^{i pi q/N} offset phase and the inverse chirp
-  for (int bin = gtid; bin < N; bin += a.gsize) {
-    double2 v = (bin < k) ? buf[swz(bin)] : buf[swz(M - N + bin)];
-    v = cmul(v, __ldg(&T.ph2[bin]));
-    buf[swz(bin)] = v;  // bins >= k read from [M-k+1, M), disjoint from [k, N)
+  for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
+    double2 ph[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = b0 + u * a.gsize;
+      ph[u] = (bin < N) ? __ldg(&T.ph2[bin]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = b0 + u * a.gsize;
+      if (bin >= N) continue;
+      // bins >= k read from [M-k+1, M), disjoint from the written range [k, N)
+      const double2 v = (bin < k) ? buf[swz(bin)] : buf[swz(M - N + bin)];
+      buf[swz(bin)] = cmul(v, ph[u]);
+    }
   }
   __syncthreads();
   for (int n = N + gtid; n < M; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 6. inverse DFT_N (Bluestein), keep the first k rings
-  fft_fwd(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
   pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
   __syncthreads();
-  fft_inv(buf, T.logM, T.tw, gtid, a.gsize);
+  fft_inv(buf, T.logM, oct, gtid, a.gsize);
   if (!valid) return;
   double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
-  for (int t = gtid; t < k; t += a.gsize) H[t] = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
+  for (int t0 = gtid; t0 < k; t0 += 8 * a.gsize) {
+    double2 c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * a.gsize;
+      c[u] = (t < k) ? __ldg(&T.chirp[t]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * a.gsize;
+      if (t < k) H[t] = cmulc(buf[swz(t)], c[u]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -182,7 +266,7 @@ static void fft_geometry(int logM, int max_rows_smem, int& gsize, int& rpc, size
   while (rpc * gsize < 128 && (size_t)(rpc * 2) * M * sizeof(double2) <= 64 * 1024 &&
          rpc * 2 <= max_rows_smem)
     rpc *= 2;
-  smem = (size_t)rpc * M * sizeof(double2);
+  smem = ((size_t)rpc * M + (M / 8 + 1)) * sizeof(double2);
 }
 
 static cudaError_t set_smem(const void* fn, size_t smem) {

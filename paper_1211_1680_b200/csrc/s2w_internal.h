@@ -10,7 +10,7 @@ namespace s2w {
 // inverse FFT.
 struct FftTablesDev {
   int N, logM;
-  const double2* tw;      // [M]  exp(-2 pi i j/M)
+  const double2* oct;     // [M/8+1] (cos, sin)(2 pi r/M): octant twiddle table
   const double2* chirp;   // [N]  c_n = exp(-i pi n^2/N)
   const double2* bl_fwd;  // [M]  FFT(conj c, circular)/M
   const double2* bl_inv;  // [M]  FFT(c, circular)/M

@@ -1,0 +1,27 @@
+"""Accuracy diagnostics on the GPU: SHT and wavelet round trips per stage."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1211_1680_b200 as sw  # noqa: E402
+from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform  # noqa: E402
+
+for L in [int(a) for a in (sys.argv[1:] or ["256", "1024", "2048"])]:
+    rng = np.random.default_rng(L)
+    f = sw.gaussian_coeffs(L, rng, real_signal=False).coeffs
+    ft = torch.from_numpy(f[None]).cuda()
+    for scheme in (sw.SamplingScheme.GL, sw.SamplingScheme.MW):
+        sht = SphericalHarmonicTransform(scheme, L)
+        x = sht.synthesis(ft)
+        back = sht.analysis(x)
+        e = (back - ft).abs().max().item()
+        print(f"L={L} {scheme.value} SHT round trip max|df|={e:.2e} (|f|max={np.abs(f).max():.1f})")
+        cfg = sw.TransformConfig(L, 2.0, 0, scheme=scheme, multires=True)
+        wt = WaveletTransform(cfg)
+        y = wt.round_trip(x)
+        fb = sht.analysis(y)
+        print(f"   wavelet rt: map rel {((y-x).abs().max()/x.abs().max()).item():.2e}  "
+              f"flm abs {(fb-ft).abs().max().item():.2e}")
