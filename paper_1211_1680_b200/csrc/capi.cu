@@ -242,14 +242,34 @@ static void fft_ld(std::vector<cld>& a) {
 
 static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
 
-// spectrum (natural order) / M, stored at bit-reversed positions
+// spectrum (natural order) / M, stored at bit-reversed positions.  Split mode
+// (M > 2^FFT_MAX_LOGM_SMEM): [even half | odd half], each bit-reversed over M/2.
 static std::vector<double2> spectrum_brev(std::vector<cld> a) {
   const size_t M = a.size();
   const int bits = ilog2_ceil((long long)M);
   fft_ld(a);
   std::vector<double2> out(M);
-  for (size_t p = 0; p < M; ++p) out[p] = d2(a[bitrev((unsigned)p, bits)] / (ld)M);
+  if (bits <= FFT_MAX_LOGM_SMEM) {
+    for (size_t p = 0; p < M; ++p) out[p] = d2(a[bitrev((unsigned)p, bits)] / (ld)M);
+  } else {
+    const size_t F = M / 2;
+    for (size_t p = 0; p < F; ++p) {
+      const size_t k = bitrev((unsigned)p, bits - 1);
+      out[p] = d2(a[2 * k] / (ld)M);
+      out[F + p] = d2(a[2 * k + 1] / (ld)M);
+    }
+  }
   return out;
+}
+
+static std::vector<double2> octant_table(int logM) {
+  const int M = 1 << logM;
+  std::vector<double2> oct(M / 8 + 1);
+  for (int j = 0; j <= M / 8; ++j) {
+    ld ang = 2.0L * PI_L * (ld)j / (ld)M;
+    oct[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
+  }
+  return oct;
 }
 
 // ------------------------------------------------------------------ per-device seed table
@@ -289,7 +309,7 @@ struct GridRes {
   std::vector<int2> act_host;
   double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
   int2* act = nullptr;
-  double2 *oct = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
+  double2 *oct = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
   double* seed_c = nullptr;
 
@@ -298,6 +318,7 @@ struct GridRes {
     t.N = N;
     t.logM = logM;
     t.oct = oct;
+    t.octM = octM;
     t.chirp = chirp;
     t.bl_fwd = bl_fwd;
     t.bl_inv = bl_inv;
@@ -388,11 +409,9 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->act, g->act_host));
 
   // FFT / Bluestein / theta-stage tables
-  std::vector<double2> oct(M / 8 + 1), chirp(N), ph1(N), ph2(N);
-  for (int j = 0; j <= M / 8; ++j) {
-    ld ang = 2.0L * PI_L * (ld)j / (ld)M;
-    oct[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
-  }
+  std::vector<double2> chirp(N), ph1(N), ph2(N);
+  const bool split = g->logM > FFT_MAX_LOGM_SMEM;
+  std::vector<double2> oct = octant_table(split ? g->logM - 1 : g->logM);
   std::vector<cld> cl(N);
   for (int n = 0; n < N; ++n) {
     long long r = ((long long)n * n) % (2LL * N);
@@ -420,6 +439,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     ph2[bin] = d2(cld(std::cos(-a1), std::sin(-a1)) * std::conj(cl[bin]));
   }
   CHECK(upload_new(&g->oct, oct));
+  if (split) CHECK(upload_new(&g->octM, octant_table(g->logM)));
   CHECK(upload_new(&g->chirp, chirp));
   CHECK(upload_new(&g->bl_fwd, spectrum_brev(b)));
   CHECK(upload_new(&g->bl_inv, spectrum_brev(cc)));
@@ -609,8 +629,9 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
 // ------------------------------------------------------------------ shared pipeline steps
 // map [n_sets][k][N] -> H [n_sets][mi][k] (m-major; MW: theta stage applied)
 static int forward_rings(const GridRes* g, int n_sets, bool real, const double* map,
-                         double2* G, cudaStream_t st) {
+                         double2* G, double2* scratch, cudaStream_t st) {
   PhiFwdArgs pa;
+  pa.scratch = scratch;
   pa.T = g->fft();
   pa.n_sets = n_sets;
   pa.n_rings = g->k;
@@ -631,6 +652,7 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
     ta.n_bins = g->n_bins(!real);
     ta.in = G;
     ta.out = G;
+    ta.scratch = scratch;
     ProfScope ps(P_THETA, st);
     CU(launch_theta(ta, st));
   }
@@ -639,8 +661,9 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
 
 // G ring-major [n_sets][k][n_bins] -> map [n_sets][k][N]
 static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
-                         cudaStream_t st) {
+                         double2* scratch, cudaStream_t st) {
   PhiInvArgs pa;
+  pa.scratch = scratch;
   pa.T = g->fft();
   pa.n_sets = n_sets;
   pa.n_rings = g->k;
@@ -658,7 +681,7 @@ static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2*
 struct s2w_sht_plan {
   int device, scheme, L;
   GridRes* g;
-  DevBuf G;
+  DevBuf G, scratch;
   SynthCfg syn;
   AnaCfg ana;
 };
@@ -709,6 +732,7 @@ int s2w_sht_plan_create(int scheme, int L, int device, s2w_sht_plan** plan) {
   p->scheme = scheme;
   p->L = L;
   int r = get_grid(device, scheme, L, &p->g);
+  if (r == S2W_OK) r = p->scratch.ensure(sizeof(double2) * fft_split_scratch_elems(p->g->logM));
   if (r != S2W_OK) {
     delete p;
     return r;
@@ -760,7 +784,7 @@ int s2w_sh_synthesis(s2w_sht_plan* p, int n_sets, int L_coef, int is_real, const
   }
   double2* bufs[S2W_NBUF] = {(double2*)flm, p->G.as<double2>(), nullptr, nullptr};
   CHECK(run_synth(c, g->seed_c, bufs, st));
-  CHECK(inverse_rings(g, n_sets, !cplx, p->G.as<double2>(), map, st));
+  CHECK(inverse_rings(g, n_sets, !cplx, p->G.as<double2>(), map, p->scratch.as<double2>(), st));
   return S2W_OK;
 }
 
@@ -794,7 +818,7 @@ int s2w_sh_analysis(s2w_sht_plan* p, int n_sets, int is_real, const double* map,
     c.key[0] = n_sets;
     c.key[1] = is_real;
   }
-  CHECK(forward_rings(g, n_sets, !cplx, map, p->G.as<double2>(), st));
+  CHECK(forward_rings(g, n_sets, !cplx, map, p->G.as<double2>(), p->scratch.as<double2>(), st));
   CU(cudaMemsetAsync(flm, 0, sizeof(double2) * (size_t)n_sets * k * k, st));
   double2* bufs[S2W_NBUF] = {(double2*)flm, p->G.as<double2>(), nullptr, nullptr};
   CHECK(run_ana(c, g->seed_c, bufs, st));
@@ -811,7 +835,7 @@ struct s2w_wav_plan {
   GridRes* top = nullptr;             // grid at L
   std::vector<GridRes*> kgrid;        // grid per kernel index
   std::vector<long long> goff;        // offset (double2) of scale j's G block in Gs
-  DevBuf f, Gtop, Gs;
+  DevBuf f, Gtop, Gs, scratch;
   SynthCfg syn_top, syn_scales;
   AnaCfg ana_top, ana_scales;
   double2* bufs() const { return nullptr; }
@@ -867,6 +891,8 @@ int s2w_wav_plan_create(int scheme, int L, int batch, int is_real, int n_kern,
   if ((r = p->Gtop.ensure(sizeof(double2) * (size_t)batch * p->top->n_bins(cplx) * L)) != S2W_OK)
     return bail(r);
   if ((r = p->Gs.ensure(sizeof(double2) * (size_t)off)) != S2W_OK) return bail(r);
+  if ((r = p->scratch.ensure(sizeof(double2) * fft_split_scratch_elems(p->top->logM))) != S2W_OK)
+    return bail(r);
 
   // slots: 0 = f, 1 = Gtop, 2 = Gs
   const int nbL = p->top->n_bins(cplx);
@@ -1008,14 +1034,15 @@ int s2w_wav_analysis_pixel(s2w_wav_plan* p, const double* map, double* const* sc
   double2* bufs[S2W_NBUF] = {p->f.as<double2>(), p->Gtop.as<double2>(), p->Gs.as<double2>(),
                              nullptr};
   // sh_analysis at L (transform.py:186)
-  CHECK(forward_rings(p->top, p->B, !cplx, map, p->Gtop.as<double2>(), st));
+  CHECK(forward_rings(p->top, p->B, !cplx, map, p->Gtop.as<double2>(), p->scratch.as<double2>(),
+                      st));
   CU(cudaMemsetAsync(p->f.p, 0, sizeof(double2) * (size_t)p->B * p->L * p->L, st));
   CHECK(run_ana(p->ana_top, p->top->seed_c, bufs, st));
   // tiling + truncation fused into the grouped per-scale synthesis (transform.py:187-190)
   CHECK(run_synth(p->syn_scales, p->top->seed_c, bufs, st));
   for (int j = 0; j < p->nk; ++j)
     CHECK(inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
-                        st));
+                        p->scratch.as<double2>(), st));
   return S2W_OK;
 }
 
@@ -1031,13 +1058,14 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, do
   // per-scale analysis (transform.py:196)
   for (int j = 0; j < p->nk; ++j)
     CHECK(forward_rings(p->kgrid[j], p->B, !cplx, scale_maps[j], p->Gs.as<double2>() + p->goff[j],
-                        st));
+                        p->scratch.as<double2>(), st));
   CU(cudaMemsetAsync(p->f.p, 0, sizeof(double2) * (size_t)p->B * p->L * p->L, st));
   // recombination (transform.py:197-199) fused into the analysis reduction
   CHECK(run_ana(p->ana_scales, p->top->seed_c, bufs, st));
   // sh_synthesis at L (transform.py:200)
   CHECK(run_synth(p->syn_top, p->top->seed_c, bufs, st));
-  CHECK(inverse_rings(p->top, p->B, !cplx, p->Gtop.as<double2>(), map, st));
+  CHECK(inverse_rings(p->top, p->B, !cplx, p->Gtop.as<double2>(), map, p->scratch.as<double2>(),
+                      st));
   return S2W_OK;
 }
 
@@ -1098,13 +1126,17 @@ int s2w_dmma_peak(double* tflops, void* stream) {
 // (include/s2w_testing.h).  Same kernels as the transforms above.
 extern "C" {
 
+static DevBuf g_test_scratch;
+
 int s2w_test_rings_inverse(int scheme, int L, int n_sets, int is_real, const double* G,
                            double* map, void* stream) {
   int dev;
   CU(cudaGetDevice(&dev));
   GridRes* g;
   CHECK(get_grid(dev, scheme, L, &g));
-  return inverse_rings(g, n_sets, is_real != 0, (const double2*)G, map, (cudaStream_t)stream);
+  CHECK(g_test_scratch.ensure(sizeof(double2) * fft_split_scratch_elems(g->logM)));
+  return inverse_rings(g, n_sets, is_real != 0, (const double2*)G, map,
+                       g_test_scratch.as<double2>(), (cudaStream_t)stream);
 }
 
 int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta_stage,
@@ -1122,6 +1154,8 @@ int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta
   pa.out = (double2*)G;
   pa.n_bins = g->n_bins(!is_real);
   pa.scale = 1.0 / (double)g->N;
+  CHECK(g_test_scratch.ensure(sizeof(double2) * fft_split_scratch_elems(g->logM)));
+  pa.scratch = g_test_scratch.as<double2>();
   {
     ProfScope ps(P_PHI_FWD, (cudaStream_t)stream);
     CU(launch_phi_fwd(pa, (cudaStream_t)stream));
@@ -1134,6 +1168,7 @@ int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta
     ta.n_bins = g->n_bins(!is_real);
     ta.in = (double2*)G;
     ta.out = (double2*)G;
+    ta.scratch = g_test_scratch.as<double2>();
     ProfScope ps(P_THETA, (cudaStream_t)stream);
     CU(launch_theta(ta, (cudaStream_t)stream));
   }

@@ -256,6 +256,200 @@ __global__ void theta_kernel(ThetaArgs a) {
   }
 }
 
+
+// =====================================================================
+// Split mode for M > 8192 (L > 2048): the length-M cyclic convolution is
+// done as two shared-memory FFT pairs of length F = M/2 (DIF first stage
+// s_j = a_j + a_{j+F}, d_j = (a_j - a_{j+F}) W_M^j; even / odd spectra),
+// with the even half kept in a per-CTA global scratch (L2-resident):
+//     y_j = u_j + W_M^-j v_j,   y_{j+F} = u_j - W_M^-j v_j.
+// One row per CTA, persistent over rows.  Spectrum tables are stored as
+// [even half | odd half], each bit-reversed over F.
+// =====================================================================
+constexpr int SPLIT_T = 512;
+
+template <class Fill>
+S2W_DEV void split_conv(double2* buf, double2* u_out, const double2* __restrict__ tab,
+                        int logF, const double2* octF, Fill fill) {
+  const int F = 1 << logF;
+  for (int half = 0; half < 2; ++half) {
+    fill(half);
+    __syncthreads();
+    fft_fwd(buf, logF, octF, threadIdx.x, SPLIT_T);
+    pointwise_mul(buf, F, tab + half * F, threadIdx.x, SPLIT_T);
+    __syncthreads();
+    fft_inv(buf, logF, octF, threadIdx.x, SPLIT_T);
+    if (half == 0) {
+      for (int j = threadIdx.x; j < F; j += SPLIT_T) u_out[j] = buf[swz(j)];
+      __syncthreads();
+    }
+  }
+}
+
+S2W_DEV double2 wM(int j, const double2* octM, int logM) { return twiddle(j, octM, logM); }
+
+__global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
+  double2* buf = smem;
+  double2* octF = smem + F;
+  double2* octM = octF + (F / 8 + 1);
+  load_octant(octF, T.oct, logF);
+  load_octant(octM, T.octM, logM);
+  double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
+  const int n_rows = a.n_sets * a.n_rings;
+  __syncthreads();
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const int set = row / a.n_rings, t = row - set * a.n_rings;
+    const long long in_base = ((long long)set * a.n_rings + t) * N;
+    split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
+      for (int j = threadIdx.x; j < F; j += SPLIT_T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (j < N) {
+          v = cmul(load_map_elem(a.in, in_base + j, a.real), __ldg(&T.chirp[j]));
+          if (half) v = cmul(v, wM(j, octM, logM));
+        }
+        buf[swz(j)] = v;
+      }
+    });
+    double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
+    for (int mi = threadIdx.x; mi < a.n_bins; mi += SPLIT_T) {
+      const double2 y = cadd(u[mi], cmulc(buf[swz(mi)], wM(mi, octM, logM)));
+      out[(size_t)mi * a.n_rings + t] = cscale(cmul(__ldg(&T.chirp[mi]), y), a.scale);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
+  double2* buf = smem;
+  double2* octF = smem + F;
+  double2* octM = octF + (F / 8 + 1);
+  load_octant(octF, T.oct, logF);
+  load_octant(octM, T.octM, logM);
+  double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
+  const int n_rows = a.n_sets * a.n_rings;
+  __syncthreads();
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const int set = row / a.n_rings, t = row - set * a.n_rings;
+    const double2* G = a.in + ((size_t)set * a.n_rings + t) * a.n_bins;
+    split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N) {
+          if (!a.real) {
+            v = __ldg(&G[n]);
+          } else if (n < a.n_bins) {
+            v = __ldg(&G[n]);
+            if (n == 0) v.y = 0.0;
+          } else {
+            v = cconj(__ldg(&G[N - n]));
+          }
+          v = cmulc(v, __ldg(&T.chirp[n]));
+          if (half) v = cmul(v, wM(n, octM, logM));
+        }
+        buf[swz(n)] = v;
+      }
+    });
+    const bool pole = a.mw_pole && t == a.n_rings - 1;
+    const double2 pv = pole ? __ldg(&G[0]) : make_double2(0.0, 0.0);
+    const size_t ob = ((size_t)set * a.n_rings + t) * N;
+    for (int p = threadIdx.x; p < N; p += SPLIT_T) {
+      const double2 y = cadd(u[p], cmulc(buf[swz(p)], wM(p, octM, logM)));
+      const double2 v = pole ? pv : cmulc(y, __ldg(&T.chirp[p]));
+      if (a.real) a.out[ob + p] = v.x;
+      else reinterpret_cast<double2*>(a.out)[ob + p] = v;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N, k = a.k;
+  const int M = 1 << logM;
+  double2* buf = smem;
+  double2* octF = smem + F;
+  double2* octM = octF + (F / 8 + 1);
+  load_octant(octF, T.oct, logF);
+  load_octant(octM, T.octM, logM);
+  double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;   // even-half results
+  double2* sv = u + F;                                  // saved row (a_bin, then X_bin)
+  const int n_rows = a.n_sets * a.n_bins;
+  __syncthreads();
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const int set = row / a.n_bins, mi = row - set * a.n_bins;
+    const int m = (mi < k) ? mi : mi - N;
+    const double sgn = (m & 1) ? -1.0 : 1.0;
+    const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
+    // 1-2. DFT_N of the parity extension (Bluestein)
+    split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N) {
+          v = (n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn);
+          v = cmul(v, __ldg(&T.chirp[n]));
+          if (half) v = cmul(v, wM(n, octM, logM));
+        }
+        buf[swz(n)] = v;
+      }
+    });
+    // 3. a_bin = y_bin ph1_bin (saved for both halves of the next convolution)
+    for (int b = threadIdx.x; b < N; b += SPLIT_T) {
+      const double2 y = cadd(u[b], cmulc(buf[swz(b)], wM(b, octM, logM)));
+      sv[b] = cmul(y, __ldg(&T.ph1[b]));
+    }
+    __syncthreads();
+    // 4. |sin| convolution of A (A_q = a_q for q < k, A_{M-N+b} = a_b for b >= k)
+    split_conv(buf, u, T.wconv, logF, octF, [&](int half) {
+      for (int j = threadIdx.x; j < F; j += SPLIT_T) {
+        double2 v = make_double2(0.0, 0.0);
+        double sign = 1.0;
+        if (j < k) {
+          v = sv[j];
+        } else if (j >= F - k + 1) {
+          v = sv[j - F + N];  // A_{j+F}
+          sign = -1.0;
+        }
+        if (half) v = cscale(cmul(v, wM(j, octM, logM)), sign);
+        buf[swz(j)] = v;
+      }
+    });
+    // 5. X_bin = H'(q) e^{i pi q/N} conj(c_bin); q = bin (bin < k) or bin - N
+    for (int b = threadIdx.x; b < N; b += SPLIT_T) {
+      double2 h;
+      if (b < k) {
+        h = cadd(u[b], cmulc(buf[swz(b)], wM(b, octM, logM)));
+      } else {
+        const int j = F + b - N;  // position M + q = j + F
+        h = csub(u[j], cmulc(buf[swz(j)], wM(j, octM, logM)));
+      }
+      sv[b] = cmul(h, __ldg(&T.ph2[b]));
+    }
+    __syncthreads();
+    // 6. inverse DFT_N (Bluestein), first k rings
+    split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) {
+        double2 v = (n < N) ? sv[n] : make_double2(0.0, 0.0);
+        if (half && n < N) v = cmul(v, wM(n, octM, logM));
+        buf[swz(n)] = v;
+      }
+    });
+    double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
+    for (int t = threadIdx.x; t < k; t += SPLIT_T) {
+      const double2 z = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
+      H[t] = cmulc(z, __ldg(&T.chirp[t]));
+    }
+    __syncthreads();
+    (void)M;
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static void fft_geometry(int logM, int max_rows_smem, int& gsize, int& rpc, size_t& smem) {
   const int M = 1 << logM;
@@ -273,9 +467,40 @@ static cudaError_t set_smem(const void* fn, size_t smem) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+static int split_grid(int n_rows) {
+  int dev, sms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return n_rows < sms ? n_rows : sms;
+}
+
+static size_t split_smem(int logM) {
+  const int F = 1 << (logM - 1);
+  return ((size_t)F + (F / 8 + 1) + ((1 << logM) / 8 + 1)) * sizeof(double2);
+}
+
+template <class Args>
+static cudaError_t split_launch(void (*kern)(Args), Args a, int n_rows, cudaStream_t st) {
+  const size_t smem = split_smem(a.T.logM);
+  cudaError_t e = set_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  if (!a.scratch) return cudaErrorInvalidValue;
+  kern<<<split_grid(n_rows), SPLIT_T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+size_t fft_split_scratch_elems(int logM) {
+  if (logM <= FFT_MAX_LOGM_SMEM) return 0;
+  int dev, sms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (size_t)sms * 2 * ((size_t)1 << (logM - 1));
+}
+
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_rings;
   if (n_rows == 0) return cudaSuccess;
+  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_fwd_split_kernel, a, n_rows, st);
   size_t smem;
   fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
   cudaError_t e = set_smem((const void*)phi_fwd_kernel, smem);
@@ -288,6 +513,7 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_rings;
   if (n_rows == 0) return cudaSuccess;
+  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_inv_split_kernel, a, n_rows, st);
   size_t smem;
   fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
   cudaError_t e = set_smem((const void*)phi_inv_kernel, smem);
@@ -300,6 +526,7 @@ cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_bins;
   if (n_rows == 0) return cudaSuccess;
+  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(theta_split_kernel, a, n_rows, st);
   size_t smem;
   fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
   cudaError_t e = set_smem((const void*)theta_kernel, smem);

@@ -8,9 +8,12 @@ namespace s2w {
 // Per grid band k (N = 2k-1, M = 2^logM >= 2N-1).  All spectra are stored in
 // bit-reversed order (see fft.cuh) and carry the 1/M of the unnormalised
 // inverse FFT.
+constexpr int FFT_MAX_LOGM_SMEM = 13;  // one 128 KiB row per CTA; larger M uses split mode
+
 struct FftTablesDev {
-  int N, logM;
-  const double2* oct;     // [M/8+1] (cos, sin)(2 pi r/M): octant twiddle table
+  int N, logM;  // logM of the convolution length M; split mode when logM > 13
+  const double2* oct;     // octant twiddle table of the FFT engine size (M, or M/2 in split mode)
+  const double2* octM;    // split mode: octant table of M (for W_M^j)
   const double2* chirp;   // [N]  c_n = exp(-i pi n^2/N)
   const double2* bl_fwd;  // [M]  FFT(conj c, circular)/M
   const double2* bl_inv;  // [M]  FFT(c, circular)/M
@@ -27,6 +30,7 @@ struct PhiFwdArgs {
   int n_bins;
   double scale;
   int gsize, rpc;  // filled by the launcher
+  double2* scratch;  // split mode: per-CTA scratch (fft_split_scratch_elems)
 };
 
 struct PhiInvArgs {
@@ -36,6 +40,7 @@ struct PhiInvArgs {
   double* out;        // [set][ring][N]
   int n_bins;
   int gsize, rpc;
+  double2* scratch;
 };
 
 struct ThetaArgs {
@@ -44,9 +49,12 @@ struct ThetaArgs {
   const double2* in;  // [set][mi][k]
   double2* out;       // [set][mi][k] (may alias in)
   int gsize, rpc;
+  double2* scratch;
 };
 
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
+// Scratch (double2 elements) the split-mode kernels need for convolution size 2^logM.
+size_t fft_split_scratch_elems(int logM);
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st);
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st);
 

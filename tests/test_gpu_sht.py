@@ -173,3 +173,18 @@ def test_multi_window_multi_pass_vs_oracle(sw, scheme, real, L):
         assert np.abs(got - want).max() <= 1e-10 * scale / N
     rec = sw.sh_analysis(m)
     assert np.abs(rec.coeffs - f.coeffs).max() <= 1e-10
+
+
+@pytest.mark.parametrize("scheme", ["GL", "MW"])
+@pytest.mark.parametrize("real,L", [(False, 2049), (True, 3001), (True, 4096), (False, 4096)])
+def test_split_fft_sizes_round_trip(sw, scheme, real, L):
+    """L > 2048 uses the split (two half-length) FFT convolutions: M = 16384."""
+    import torch
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform
+
+    rng = np.random.default_rng(L)
+    f = sw.gaussian_coeffs(L, rng, real_signal=real).coeffs
+    sht = SphericalHarmonicTransform(getattr(sw.SamplingScheme, scheme), L)
+    x = sht.synthesis(torch.from_numpy(f[None].copy()).cuda(), real=real)
+    back = sht.analysis(x).cpu().numpy()[0]
+    assert np.abs(back - f).max() <= 2e-10 * max(1.0, np.abs(f).max())

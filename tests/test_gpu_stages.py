@@ -80,3 +80,22 @@ def test_theta_stage_vs_oracle(env, L, real):
     scale = np.abs(Href).max()
     # rows t < L-1 agree; at the pole the symmetrised H is 2x (even m) or 0 (odd m)
     assert np.abs(H[:, :, :-1] - Href[:, :, :-1]).max() <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("L", [2049, 4096])
+@pytest.mark.parametrize("real", [True, False])
+def test_phi_stages_split_mode_vs_numpy(env, L, real):
+    rng = np.random.default_rng(L)
+    N = 2 * L - 1
+    nb = L if real else N
+    G = rng.standard_normal((1, L, nb)) + 1j * rng.standard_normal((1, L, nb))
+    if real:
+        G[:, :, 0] = G[:, :, 0].real
+        want = np.fft.irfft(G, n=N, axis=-1, norm="forward")
+    else:
+        want = np.fft.ifft(G, axis=-1, norm="forward")
+    got = _run_inverse(env, 0, L, G, real)
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max() * np.log2(N)
+    F = (np.fft.rfft(want, axis=-1) if real else np.fft.fft(want, axis=-1)) / N
+    got_f = _run_forward(env, 0, L, want if not real else want.astype(complex), real, 0)
+    assert np.abs(got_f - np.swapaxes(F, 1, 2)).max() <= 1e-14 * np.abs(F).max() * np.log2(N)
