@@ -12,7 +12,8 @@ from pathlib import Path
 
 from .errors import ParameterError, SphwavError
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libs2w.so"
+_LIB_PATH = Path(os.environ.get("S2W_LIB") or
+                 Path(__file__).resolve().parent / "lib" / "libs2w.so")
 
 S2W_OK, S2W_EPARAM = 0, 1
 SCHEME_GL, SCHEME_MW = 0, 1

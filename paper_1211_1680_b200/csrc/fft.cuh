@@ -260,3 +260,47 @@ S2W_DEV void pointwise_mul(double2* buf, int M, const double2* __restrict__ tab,
     }
   }
 }
+
+// Cyclic convolution core: forward DIF FFT, pointwise product with the
+// bit-reversed table, inverse DIT FFT -- with the last forward pass, the
+// product and the first inverse pass (all of span 1 over blocks of R
+// contiguous elements, no twiddles) fused into one shared-memory pass.
+// Precondition: row written and synced.  Ends with a __syncthreads.
+template <int R>
+S2W_DEV void conv_core_pass(double2* __restrict__ buf, int M, const double2* __restrict__ tab,
+                            int gtid, int gsize) {
+  for (int b = gtid; b < M / R; b += gsize) {
+    double2 v[R], t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[swz(b * R + i)];
+    bfly_fwd<R>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], t[i]);
+    bfly_inv<R>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[swz(b * R + i)] = v[i];
+  }
+}
+
+S2W_DEV void fft_conv(double2* buf, int logM, const double2* __restrict__ oct,
+                      const double2* __restrict__ tab, int gtid, int gsize) {
+  const int M = 1 << logM;
+  const int rem = logM % 3;
+  const int lastR = rem == 0 ? 8 : (1 << rem);
+  const int lastl = rem == 0 ? 3 : rem;
+  // forward: radix-8 passes down to span lastR
+  for (int ls = logM - 3; ls >= lastl; ls -= 3) {
+    fft_pass<8, false>(buf, logM, ls, oct, gtid, gsize);
+    __syncthreads();
+  }
+  if (lastR == 8) conv_core_pass<8>(buf, M, tab, gtid, gsize);
+  else if (lastR == 4) conv_core_pass<4>(buf, M, tab, gtid, gsize);
+  else conv_core_pass<2>(buf, M, tab, gtid, gsize);
+  __syncthreads();
+  for (int ls = lastl; ls < logM; ls += 3) {
+    fft_pass<8, true>(buf, logM, ls, oct, gtid, gsize);
+    __syncthreads();
+  }
+}

@@ -57,10 +57,7 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
     }
   }
   __syncthreads();
-  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
-  pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
-  __syncthreads();
-  fft_inv(buf, T.logM, oct, gtid, a.gsize);
+  fft_conv(buf, T.logM, oct, T.bl_fwd, gtid, a.gsize);
   if (!valid) return;
   double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
   for (int m0 = gtid; m0 < a.n_bins; m0 += 8 * a.gsize) {
@@ -121,10 +118,7 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
     }
   }
   __syncthreads();
-  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
-  pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
-  __syncthreads();
-  fft_inv(buf, T.logM, oct, gtid, a.gsize);
+  fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
   if (!valid) return;
   const bool pole = a.mw_pole && t == a.n_rings - 1;
   double2 pv = make_double2(0.0, 0.0);
@@ -185,10 +179,7 @@ __global__ void theta_kernel(ThetaArgs a) {
   }
   __syncthreads();
   // 2. DFT_N (Bluestein)
-  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
-  pointwise_mul(buf, M, T.bl_fwd, gtid, a.gsize);
-  __syncthreads();
-  fft_inv(buf, T.logM, oct, gtid, a.gsize);
+  fft_conv(buf, T.logM, oct, T.bl_fwd, gtid, a.gsize);
   // 3. Fourier coefficients a_{m'} = c_bin e^{-i pi m'/N} conv[bin] / N, laid out
   //    over the length-M circle (negative m' at the top)
   for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
@@ -210,10 +201,7 @@ __global__ void theta_kernel(ThetaArgs a) {
   for (int n = k + gtid; n < M - k + 1; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 4. convolution with the |sin theta| series (precomputed spectrum)
-  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
-  pointwise_mul(buf, M, T.wconv, gtid, a.gsize);
-  __syncthreads();
-  fft_inv(buf, T.logM, oct, gtid, a.gsize);
+  fft_conv(buf, T.logM, oct, T.wconv, gtid, a.gsize);
   // 5. back onto N bins with the e^{i pi q/N} offset phase and the inverse chirp
   for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
     double2 ph[8];
@@ -235,10 +223,7 @@ __global__ void theta_kernel(ThetaArgs a) {
   for (int n = N + gtid; n < M; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 6. inverse DFT_N (Bluestein), keep the first k rings
-  fft_fwd(buf, T.logM, oct, gtid, a.gsize);
-  pointwise_mul(buf, M, T.bl_inv, gtid, a.gsize);
-  __syncthreads();
-  fft_inv(buf, T.logM, oct, gtid, a.gsize);
+  fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
   if (!valid) return;
   double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
   for (int t0 = gtid; t0 < k; t0 += 8 * a.gsize) {
@@ -275,10 +260,7 @@ S2W_DEV void split_conv(double2* buf, double2* u_out, const double2* __restrict_
   for (int half = 0; half < 2; ++half) {
     fill(half);
     __syncthreads();
-    fft_fwd(buf, logF, octF, threadIdx.x, SPLIT_T);
-    pointwise_mul(buf, F, tab + half * F, threadIdx.x, SPLIT_T);
-    __syncthreads();
-    fft_inv(buf, logF, octF, threadIdx.x, SPLIT_T);
+    fft_conv(buf, logF, octF, tab + half * F, threadIdx.x, SPLIT_T);
     if (half == 0) {
       for (int j = threadIdx.x; j < F; j += SPLIT_T) u_out[j] = buf[swz(j)];
       __syncthreads();
