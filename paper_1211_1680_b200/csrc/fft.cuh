@@ -124,6 +124,12 @@ template <> S2W_DEV void bfly_inv<8>(double2* v) {
   v[7] = csub(b3, t);
 }
 
+// Octant-table slot of entry r: XOR-swizzled so that power-of-two strides
+// (tstep = 8, 64, 512 in the radix-8 passes) hit distinct 16-byte bank groups.
+S2W_DEV int oct_slot(int r) { return r ^ (((r >> 3) ^ (r >> 6) ^ (r >> 9)) & 7); }
+// entries allocated for an octant table of M = 2^logM (slot range rounded to 8)
+__host__ __device__ constexpr int oct_alloc(int logM) { return ((1 << (logM - 3)) + 8) & ~7; }
+
 // W_M^k = exp(-2 pi i k / M) from an octant table oct[r] = (cos, sin)(2 pi r / M),
 // r in [0, M/8], held in shared memory (M/8 + 1 entries: 16 KiB at M = 8192).
 S2W_DEV double2 twiddle(int k, const double2* __restrict__ oct, int logM) {
@@ -132,7 +138,7 @@ S2W_DEV double2 twiddle(int k, const double2* __restrict__ oct, int logM) {
   const int q = (k >> sh) & 7;
   int r = k & (M8 - 1);
   if (q & 1) r = M8 - r;
-  const double2 e = oct[r];
+  const double2 e = oct[oct_slot(r)];
   const bool swap = ((q + 1) & 2) != 0;          // q in {1, 2, 5, 6}
   double c = swap ? e.y : e.x;
   double s = swap ? e.x : e.y;
@@ -198,7 +204,7 @@ S2W_DEV void fft_pass(double2* __restrict__ buf, int logM, int log2s,
 // Copy the octant table (M/8 + 1 entries) from global into shared memory.
 S2W_DEV void load_octant(double2* __restrict__ s_oct, const double2* __restrict__ g_oct, int logM) {
   const int n = (1 << (logM - 3)) + 1;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s_oct[i] = __ldg(&g_oct[i]);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_oct[oct_slot(i)] = __ldg(&g_oct[i]);
 }
 
 // Forward DIF FFT: natural -> bit-reversed.  Ends with a __syncthreads.

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
   const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
   double2* buf = smem;
   double2* octF = smem + F;
-  double2* octM = octF + (F / 8 + 1);
+  double2* octM = octF + oct_alloc(logF);
   load_octant(octF, T.oct, logF);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
   const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
   double2* buf = smem;
   double2* octF = smem + F;
-  double2* octM = octF + (F / 8 + 1);
+  double2* octM = octF + oct_alloc(logF);
   load_octant(octF, T.oct, logF);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   const int M = 1 << logM;
   double2* buf = smem;
   double2* octF = smem + F;
-  double2* octM = octF + (F / 8 + 1);
+  double2* octM = octF + oct_alloc(logF);
   load_octant(octF, T.oct, logF);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;   // even-half results
@@ -442,7 +442,7 @@ static void fft_geometry(int logM, int max_rows_smem, int& gsize, int& rpc, size
   while (rpc * gsize < 128 && (size_t)(rpc * 2) * M * sizeof(double2) <= 64 * 1024 &&
          rpc * 2 <= max_rows_smem)
     rpc *= 2;
-  smem = ((size_t)rpc * M + (M / 8 + 1)) * sizeof(double2);
+  smem = ((size_t)rpc * M + oct_alloc(logM)) * sizeof(double2);
 }
 
 static cudaError_t set_smem(const void* fn, size_t smem) {
@@ -458,7 +458,7 @@ static int split_grid(int n_rows) {
 
 static size_t split_smem(int logM) {
   const int F = 1 << (logM - 1);
-  return ((size_t)F + (F / 8 + 1) + ((1 << logM) / 8 + 1)) * sizeof(double2);
+  return ((size_t)F + oct_alloc(logM - 1) + oct_alloc(logM)) * sizeof(double2);
 }
 
 template <class Args>
