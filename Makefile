@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v -Iinclude
 SRC := $(wildcard paper_1211_1680_b200/csrc/*.cu)
-HDR := $(wildcard paper_1211_1680_b200/csrc/*.cuh paper_1211_1680_b200/csrc/*.h) include/s2w.h
+HDR := $(wildcard paper_1211_1680_b200/csrc/*.cuh paper_1211_1680_b200/csrc/*.h paper_1211_1680_b200/csrc/*.inc) include/s2w.h
 LIB := paper_1211_1680_b200/lib/libs2w.so
 OBJ := $(patsubst paper_1211_1680_b200/csrc/%.cu,build/%.o,$(SRC))
 

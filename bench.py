@@ -140,34 +140,67 @@ def run_ours(args, cfgname):
 
     import paper_1211_1680_b200 as sw
     from paper_1211_1680_b200 import _native
+    from paper_1211_1680_b200 import distributed as D
     from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    mode = args.mode or ("shard" if ws > 1 else "single")
+    if ws > 1 or mode == "shard":
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"),
+                     ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     cfg = CONFIGS[cfgname]
     L, B, real = cfg["L"], cfg["batch"], cfg["real"]
     scheme = sw.SamplingScheme.MW
     tcfg = sw.TransformConfig(L, cfg["lam"], cfg["j0"], scheme=scheme, multires=cfg["multires"])
-    wt = WaveletTransform(tcfg, batch=B, real=real)
 
-    # seeded input (untimed setup): f_lm -> MW map through our own synthesis
-    flm = np.stack([seeded_coeffs(L, real, cfg["spec"], 1000 + 97 * rank + b) for b in range(B)])
+    # seeded input (untimed setup): f_lm -> MW map through our own synthesis.
+    # single / replica: every rank transforms its own map(s); shard: the ranks
+    # share ONE batch of maps, each holding its ring block.
+    seed0 = 1000 + (97 * rank if mode == "replica" else 0)
+    flm = np.stack([seeded_coeffs(L, real, cfg["spec"], seed0 + b) for b in range(B)])
     sht = SphericalHarmonicTransform(scheme, L)
-    x = sht.synthesis(torch.from_numpy(flm).cuda(), real=real)
-    scale = wt.alloc_scale_maps()
-    out = torch.empty_like(x)
+    x_full = sht.synthesis(torch.from_numpy(flm).cuda(), real=real)
     st = torch.cuda.current_stream()
 
+    if mode == "shard":
+        sh = D.ShardedWaveletTransform(tcfg, D.TorchExchange(), batch=B, real=real)
+        t0, t1 = sh.ring_block(L, rank)
+        x = x_full[:, t0:t1, :].contiguous()
+        bands = sh.bands
+
+        def step(inp):
+            return sh.round_trip({rank: inp})[rank]
+
+        maps_per_step = B  # the job transforms one batch per step
+    else:
+        wt = WaveletTransform(tcfg, batch=B, real=real)
+        x = x_full
+        bands = wt.bands
+        scale = wt.alloc_scale_maps()
+        out_buf = torch.empty_like(x)
+
+        def step(inp):
+            return wt.round_trip(inp, scale, out_buf)
+
+        maps_per_step = ws * B
+    del x_full
+
     def barrier():
-        if ws > 1:
+        if dist.is_initialized():
             dist.barrier()
 
+    out = None
     for _ in range(args.warmup):
-        wt.round_trip(x, scale, out)
+        out = step(x)
     torch.cuda.synchronize()
-    err = (out - x).abs().max().item() / x.abs().max().item()
+    err = (out - x).abs().max().item() / max(x.abs().max().item(), 1e-300)
+    if ws > 1:
+        t = torch.tensor([err], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        err = t.item()
 
     # --- device-resident timed region
     _native.profile_enable(True)
@@ -179,7 +212,7 @@ def run_ours(args, cfgname):
         torch.cuda.synchronize()
         ev0.record(st)
         for _ in range(args.steps):
-            wt.round_trip(x, scale, out)
+            out = step(x)
         ev1.record(st)
         torch.cuda.synchronize()
         barrier()
@@ -191,19 +224,19 @@ def run_ours(args, cfgname):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
-    value = ws * B * args.steps / (ms / 1e3)
+    value = maps_per_step * args.steps / (ms / 1e3)
 
     # --- end to end through the public API with pinned host buffers
     x_host = x.cpu().pin_memory()
     out_host = torch.empty_like(x_host).pin_memory()
     for _ in range(max(1, args.warmup // 2)):
-        out_host.copy_(wt.round_trip(x_host, scale, out), non_blocking=True)
+        out_host.copy_(step(x_host.cuda(non_blocking=True)), non_blocking=True)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(args.steps):
-        out_host.copy_(wt.round_trip(x_host, scale, out), non_blocking=True)
+        out_host.copy_(step(x_host.cuda(non_blocking=True)), non_blocking=True)
     e1.record(st)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
@@ -211,18 +244,21 @@ def run_ours(args, cfgname):
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = t.item()
-    e2e = ws * B * args.steps / (ms_e2e / 1e3)
+    e2e = maps_per_step * args.steps / (ms_e2e / 1e3)
     nbytes = x.numel() * x.element_size()
 
     fp64_peak = _native.fp64_peak_tflops(None)
+    dmma_peak = _native.dmma_peak_tflops(None)
     if rank != 0:
-        if ws > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return None
-    fl = stage_flops(cfg, wt.bands)
+    fl = stage_flops(cfg, bands)
     dom = max(("leg_synth", "leg_ana"), key=lambda s: prof[s][0])
     dms, dn = prof[dom]
-    achieved = fl[dom] / (dms / dn * 1e-3) / 1e12 if dn else None
+    shard_frac = 1.0 / ws if mode == "shard" else 1.0
+    achieved = fl[dom] * shard_frac / (dms / dn * 1e-3) / 1e12 if dn else None
+    peak = max(fp64_peak, dmma_peak)
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
               for k, v in prof.items()}
     rec = {
@@ -234,7 +270,7 @@ def run_ours(args, cfgname):
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if mode == "shard" else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded Gaussian f_lm, BASELINE spectrum; MW map from our synthesis)",
@@ -242,30 +278,33 @@ def run_ours(args, cfgname):
             "workload": f"{cfgname}: L={L} MW {'real' if real else 'complex'} x{B}, "
                         f"lambda={cfg['lam']:g}, J0={cfg['j0']}, "
                         f"{'multires' if cfg['multires'] else 'full-res'}",
-            "L": L, "batch": B, "bands": list(wt.bands),
-            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-            "l2": f"inputs larger than L2 (map {nbytes / 1e6:.0f} MB, working set > 1 GB)",
+            "L": L, "batch": B, "bands": list(bands),
+            "parallelism": {"single": "single GPU", "replica": f"replicas x{ws}",
+                            "shard": f"orders/rings sharded x{ws} (NCCL all-to-all)"}[mode],
+            "l2": f"inputs larger than L2 (map {nbytes * (ws if mode == 'shard' else 1) / 1e6:.0f}"
+                  " MB, working set > 1 GB)" if L >= 1024 else "small config (L2-resident)",
         },
         "e2e": {"value": e2e, "unit": "round-trips/s", "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes},
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "fp64", "kernel": dom,
-            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp64_peak if achieved else None,
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if achieved else None,
             "traffic": None,
-            "flops_per_launch": fl[dom],
-            "peak_source": "measured DFMA microbenchmark (s2w_fp64_peak) in this run; "
-                           "MEASURED_PEAKS.json has no FP64 entry",
+            "flops_per_launch": fl[dom] * shard_frac,
+            "peak_source": f"measured in this run: DFMA {fp64_peak:.1f}, DMMA {dmma_peak:.1f} "
+                           "TFLOP/s (s2w_fp64_peak / s2w_dmma_peak); MEASURED_PEAKS.json has "
+                           "no FP64 entry",
         },
         "stages": stages,
         "canonical_flops_per_rt": fl["per_rt"],
-        "fp64_tflops_per_rt": fl["per_rt"] * value / ws / 1e12,
+        "fp64_tflops_per_gpu": fl["per_rt"] * value / ws / 1e12 / B,
         "rt_rel_err": err,
         "clocks": clk.summary(),
     }
     rec["cpu_baseline"] = cpu_baseline(cfgname, args) if not args.no_cpu else None
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return rec
 
@@ -315,6 +354,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--mode", choices=["single", "shard", "replica"], default=None,
+                    help="N=1: single; N>1 default shard (one map split by orders/rings, "
+                         "strong scaling) or replica (independent maps, weak scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -120,6 +120,37 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* plan, const double* const* scale_maps,
  * s2w_wav_synthesis_pixel the recombined f_lm (transform.py:196-200). */
 int s2w_wav_plan_flm(s2w_wav_plan* plan, double** flm);
 
+/* ---------------------------------------------------------------- shards (multi-GPU) */
+/* One grid restricted to a rank's share of the work: the orders m in `orders`
+ * (Legendre and theta stages) and the ring block [t0, t1) (ring FFT stages).
+ * The exchange between the two (an all-to-all of per-ring Fourier modes) is
+ * the caller's (torch.distributed / NCCL); paper_1211_1680_b200/distributed.py
+ * drives it.  Layouts (B = batch, n_local = number of my bins: per listed order
+ * m, bin m then, for complex data and m > 0, bin 2L-1-m):
+ *   map rows [B][t1-t0][2L-1]  G_col [B][n_bins][t1-t0]  G_ring [B][t1-t0][n_bins]
+ *   G_local [B][L][n_local]    H_local [B][n_local][L]
+ * weights: optional HOST table [n_w][L] of per-degree factors (tiling). */
+typedef struct s2w_shard_plan s2w_shard_plan;
+int s2w_shard_plan_create(int scheme, int L, int batch, int is_real, int n_orders,
+                          const int* orders, int t0, int t1, int n_w, const double* weights,
+                          int device, s2w_shard_plan** plan);
+int s2w_shard_plan_destroy(s2w_shard_plan* plan);
+/* Number (and list, if bins != NULL) of my bins, in local order. */
+int s2w_shard_bins(s2w_shard_plan* plan, int* n_bins, int* bins);
+/* map rows -> G_col = DFT_phi / N (all bins, my rings). */
+int s2w_shard_rings_forward(s2w_shard_plan* plan, const double* map_rows, double* G, void* stream);
+/* G_ring -> map rows (my rings; MW pole ring pinned if it is mine). */
+int s2w_shard_rings_inverse(s2w_shard_plan* plan, const double* G, double* map_rows, void* stream);
+/* H_local in place: MW theta stage for my bins (no-op on GL grids). */
+int s2w_shard_theta(s2w_shard_plan* plan, double* H, void* stream);
+/* flm [B][flm_L^2] (x weight row w_index, -1 = none) -> G_local for my orders. */
+int s2w_shard_legendre_synthesis(s2w_shard_plan* plan, const double* flm, int flm_L, int w_index,
+                                 double* G, void* stream);
+/* H_local -> flm [B][flm_L^2] at my orders (x weight row w_index); accumulate != 0
+ * adds into flm, otherwise flm is zeroed first. */
+int s2w_shard_legendre_analysis(s2w_shard_plan* plan, const double* H, double* flm, int flm_L,
+                                int w_index, int accumulate, void* stream);
+
 /* ---------------------------------------------------------------- accounting */
 /* Number of kernels launched by this library since load (bench "gpu_launches"). */
 long long s2w_kernel_launches(void);

@@ -41,6 +41,18 @@ _PROTOS = {
     "s2w_wav_synthesis_harmonic": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_wav_analysis_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "s2w_wav_synthesis_pixel": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_shard_plan_create": (
+        _c_int,
+        [_c_int, _c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int), _c_int, _c_int, _c_int,
+         _dp, _c_int, ctypes.POINTER(_vp)],
+    ),
+    "s2w_shard_plan_destroy": (_c_int, [_vp]),
+    "s2w_shard_bins": (_c_int, [_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)]),
+    "s2w_shard_rings_forward": (_c_int, [_vp, _vp, _vp, _vp]),
+    "s2w_shard_rings_inverse": (_c_int, [_vp, _vp, _vp, _vp]),
+    "s2w_shard_theta": (_c_int, [_vp, _vp, _vp]),
+    "s2w_shard_legendre_synthesis": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
+    "s2w_shard_legendre_analysis": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp]),
     "s2w_kernel_launches": (ctypes.c_longlong, []),
     "s2w_profile_enable": (_c_int, [_c_int]),
     "s2w_profile_read": (

@@ -336,6 +336,8 @@ struct GridRes {
     g.sin_t = sin_t;
     g.ring_w = ring_w;
     g.act = act;
+    g.binmap = nullptr;
+    g.n_cols = cplx ? N : k;
     return g;
   }
   int n_bins(bool cplx) const { return cplx ? N : k; }
@@ -650,6 +652,7 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
     ta.n_sets = n_sets;
     ta.k = g->k;
     ta.n_bins = g->n_bins(!real);
+    ta.row_bin = nullptr;
     ta.in = G;
     ta.out = G;
     ta.scratch = scratch;
@@ -669,6 +672,7 @@ static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2*
   pa.n_rings = g->k;
   pa.real = real ? 1 : 0;
   pa.mw_pole = g->scheme == S2W_SCHEME_MW;
+  pa.t_offset = 0;
   pa.in = G;
   pa.out = map;
   pa.n_bins = g->n_bins(!real);
@@ -1166,6 +1170,7 @@ int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta
     ta.n_sets = n_sets;
     ta.k = g->k;
     ta.n_bins = g->n_bins(!is_real);
+    ta.row_bin = nullptr;
     ta.in = (double2*)G;
     ta.out = (double2*)G;
     ta.scratch = g_test_scratch.as<double2>();
@@ -1176,3 +1181,4 @@ int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta
 }
 
 }  // extern "C"
+#include "capi_shard.inc"

@@ -120,7 +120,7 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   __syncthreads();
   fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
   if (!valid) return;
-  const bool pole = a.mw_pole && t == a.n_rings - 1;
+  const bool pole = a.mw_pole && t + a.t_offset == (T.N + 1) / 2 - 1;
   double2 pv = make_double2(0.0, 0.0);
   if (pole) pv = __ldg(&G[0]);
   const size_t ob = ((size_t)set * a.n_rings + t) * N;
@@ -155,8 +155,9 @@ __global__ void theta_kernel(ThetaArgs a) {
   const int n_rows = a.n_sets * a.n_bins;
   const bool valid = row < n_rows;
   const int set = valid ? row / a.n_bins : 0;
-  const int mi = valid ? row - set * a.n_bins : 0;
-  const int m = (mi < k) ? mi : mi - N;
+  const int mi = valid ? row - set * a.n_bins : 0;  // storage row
+  const int bin = a.row_bin ? a.row_bin[mi] : mi;
+  const int m = (bin < k) ? bin : bin - N;
   const double sgn = (m & 1) ? -1.0 : 1.0;
   const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
 
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
         buf[swz(n)] = v;
       }
     });
-    const bool pole = a.mw_pole && t == a.n_rings - 1;
+    const bool pole = a.mw_pole && t + a.t_offset == (T.N + 1) / 2 - 1;
     const double2 pv = pole ? __ldg(&G[0]) : make_double2(0.0, 0.0);
     const size_t ob = ((size_t)set * a.n_rings + t) * N;
     for (int p = threadIdx.x; p < N; p += SPLIT_T) {
@@ -366,7 +367,8 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   __syncthreads();
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
     const int set = row / a.n_bins, mi = row - set * a.n_bins;
-    const int m = (mi < k) ? mi : mi - N;
+    const int bin = a.row_bin ? a.row_bin[mi] : mi;
+    const int m = (bin < k) ? bin : bin - N;
     const double sgn = (m & 1) ? -1.0 : 1.0;
     const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
     // 1-2. DFT_N of the parity extension (Bluestein)

@@ -36,6 +36,7 @@ struct PhiFwdArgs {
 struct PhiInvArgs {
   FftTablesDev T;
   int n_sets, n_rings, real, mw_pole;
+  int t_offset;  // global ring index of local row 0 (ring-sharded maps); pole = ring k-1
   const double2* in;  // [set][ring][n_bins]
   double* out;        // [set][ring][N]
   int n_bins;
@@ -45,7 +46,8 @@ struct PhiInvArgs {
 
 struct ThetaArgs {
   FftTablesDev T;
-  int n_sets, k, n_bins;
+  int n_sets, k, n_bins;  // n_bins = rows per set
+  const int* row_bin;     // row -> azimuthal bin (order-sharded rows); nullptr = identity
   const double2* in;  // [set][mi][k]
   double2* out;       // [set][mi][k] (may alias in)
   int gsize, rpc;
@@ -67,6 +69,8 @@ struct LegGridDev {
   const double* sin_t;
   const double* ring_w;  // analysis quadrature weight per ring (incl. 2 pi / N factors)
   const int2* act;       // [k] active ring range [lo, hi) per order m
+  const int* binmap;     // bin -> local column (synthesis) / row (analysis); nullptr = identity
+  int n_cols;            // synthesis output row stride (n_bins unless sharded by order)
 };
 
 // Buffers are addressed as (slot, element offset) into the per-launch base
