@@ -27,6 +27,8 @@ __device__ __forceinline__ double2 load_map_elem(const double* __restrict__ in, 
 
 // ---------------------------------------------------------------- phi forward
 __global__ void phi_fwd_kernel(PhiFwdArgs a) {
+  // Real maps: two rings per transform (z = x + i y; X_k = (Z_k + conj Z_{N-k})/2,
+  // Y_k = (Z_k - conj Z_{N-k})/2i), halving the FFT work.
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
   const int M = 1 << T.logM, N = T.N;
@@ -34,12 +36,14 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
   double2* buf = smem + (size_t)grp * M;
   double2* oct = smem + (size_t)a.rpc * M;
   load_octant(oct, T.oct, T.logM);
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;  // transforms per set
   const int row = blockIdx.x * a.rpc + grp;
-  const int n_rows = a.n_sets * a.n_rings;
-  const bool valid = row < n_rows;
-  const int set = valid ? row / a.n_rings : 0;
-  const int t = valid ? row - set * a.n_rings : 0;
-  const long long in_base = ((long long)set * a.n_rings + t) * N;
+  const bool valid = row < a.n_sets * per;
+  const int set = valid ? row / per : 0;
+  const int p = valid ? row - set * per : 0;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && valid && ta + 1 < a.n_rings;
+  const long long base_a = ((long long)set * a.n_rings + ta) * N;
 
   for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
     double2 x[8], c[8];
@@ -47,7 +51,13 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
     for (int u = 0; u < 8; ++u) {
       const int n = n0 + u * a.gsize;
       const bool in = valid && n < N;
-      x[u] = in ? load_map_elem(a.in, in_base + n, a.real) : make_double2(0.0, 0.0);
+      if (!a.real) {
+        x[u] = in ? __ldg(reinterpret_cast<const double2*>(a.in) + base_a + n)
+                  : make_double2(0.0, 0.0);
+      } else {
+        x[u] = make_double2(in ? __ldg(&a.in[base_a + n]) : 0.0,
+                            (in && vb) ? __ldg(&a.in[base_a + N + n]) : 0.0);
+      }
       c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
@@ -60,24 +70,24 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
   fft_conv(buf, T.logM, oct, T.bl_fwd, gtid, a.gsize);
   if (!valid) return;
   double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
-  for (int m0 = gtid; m0 < a.n_bins; m0 += 8 * a.gsize) {
-    double2 c[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int mi = m0 + u * a.gsize;
-      c[u] = (mi < a.n_bins) ? __ldg(&T.chirp[mi]) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int mi = m0 + u * a.gsize;
-      if (mi < a.n_bins)
-        out[(size_t)mi * a.n_rings + t] = cscale(cmul(c[u], buf[swz(mi)]), a.scale);
+  for (int mi = gtid; mi < a.n_bins; mi += a.gsize) {
+    const double2 z = cmul(__ldg(&T.chirp[mi]), buf[swz(mi)]);
+    if (!a.real) {
+      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+    } else {
+      const int mr = mi ? N - mi : 0;
+      const double2 zr = cconj(cmul(__ldg(&T.chirp[mr]), buf[swz(mr)]));
+      const double h = 0.5 * a.scale;
+      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
+      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
     }
   }
 }
 
 // ---------------------------------------------------------------- phi inverse
 __global__ void phi_inv_kernel(PhiInvArgs a) {
+  // Real maps: two rings per transform (Z = X + i Y of their Hermitian spectra;
+  // the two real rings are Re and Im of the inverse DFT).
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
   const int M = 1 << T.logM, N = T.N;
@@ -85,12 +95,15 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   double2* buf = smem + (size_t)grp * M;
   double2* oct = smem + (size_t)a.rpc * M;
   load_octant(oct, T.oct, T.logM);
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
   const int row = blockIdx.x * a.rpc + grp;
-  const int n_rows = a.n_sets * a.n_rings;
-  const bool valid = row < n_rows;
-  const int set = valid ? row / a.n_rings : 0;
-  const int t = valid ? row - set * a.n_rings : 0;
-  const double2* G = a.in + ((size_t)set * a.n_rings + t) * a.n_bins;
+  const bool valid = row < a.n_sets * per;
+  const int set = valid ? row / per : 0;
+  const int p = valid ? row - set * per : 0;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && valid && ta + 1 < a.n_rings;
+  const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * a.n_bins;
+  const double2* Gb = Ga + a.n_bins;
 
   for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
     double2 x[8], c[8];
@@ -101,12 +114,19 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
       c[u] = make_double2(0.0, 0.0);
       if (valid && n < N) {
         if (!a.real) {
-          x[u] = __ldg(&G[n]);
-        } else if (n < a.n_bins) {
-          x[u] = __ldg(&G[n]);
-          if (n == 0) x[u].y = 0.0;  // irfft ignores Im of the DC bin
+          x[u] = __ldg(&Ga[n]);
         } else {
-          x[u] = cconj(__ldg(&G[N - n]));
+          // Hermitian spectra of the two rings (irfft ignores Im of the DC bin)
+          double2 X, Y = make_double2(0.0, 0.0);
+          if (n < a.n_bins) {
+            X = __ldg(&Ga[n]);
+            if (vb) Y = __ldg(&Gb[n]);
+            if (n == 0) X.y = Y.y = 0.0;
+          } else {
+            X = cconj(__ldg(&Ga[N - n]));
+            if (vb) Y = cconj(__ldg(&Gb[N - n]));
+          }
+          x[u] = cadd(X, cmul_pi(Y));
         }
         c[u] = __ldg(&T.chirp[n]);
       }
@@ -120,24 +140,18 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   __syncthreads();
   fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
   if (!valid) return;
-  const bool pole = a.mw_pole && t + a.t_offset == (T.N + 1) / 2 - 1;
-  double2 pv = make_double2(0.0, 0.0);
-  if (pole) pv = __ldg(&G[0]);
-  const size_t ob = ((size_t)set * a.n_rings + t) * N;
-  for (int p0 = gtid; p0 < N; p0 += 8 * a.gsize) {
-    double2 c[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = p0 + u * a.gsize;
-      c[u] = (p < N) ? __ldg(&T.chirp[p]) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = p0 + u * a.gsize;
-      if (p >= N) continue;
-      const double2 v = pole ? pv : cmulc(buf[swz(p)], c[u]);
-      if (a.real) a.out[ob + p] = v.x;
-      else reinterpret_cast<double2*>(a.out)[ob + p] = v;
+  const int pole_ring = (T.N + 1) / 2 - 1 - a.t_offset;  // local index of the MW pole ring
+  const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
+  const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
+  const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
+  const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+  for (int q = gtid; q < N; q += a.gsize) {
+    const double2 v = cmulc(buf[swz(q)], __ldg(&T.chirp[q]));
+    if (a.real) {
+      a.out[ob + q] = pa ? pva.x : v.x;
+      if (vb) a.out[ob + N + q] = pb ? pvb.x : v.y;
+    } else {
+      reinterpret_cast<double2*>(a.out)[ob + q] = pa ? pva : v;
     }
   }
 }
@@ -281,16 +295,21 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
   load_octant(octF, T.oct, logF);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
-  const int n_rows = a.n_sets * a.n_rings;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int n_rows = a.n_sets * per;
   __syncthreads();
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
-    const int set = row / a.n_rings, t = row - set * a.n_rings;
-    const long long in_base = ((long long)set * a.n_rings + t) * N;
+    const int set = row / per, p = row - set * per;
+    const int ta = a.real ? 2 * p : p;
+    const bool vb = a.real && ta + 1 < a.n_rings;
+    const long long base_a = ((long long)set * a.n_rings + ta) * N;
     split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
       for (int j = threadIdx.x; j < F; j += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (j < N) {
-          v = cmul(load_map_elem(a.in, in_base + j, a.real), __ldg(&T.chirp[j]));
+          if (!a.real) v = __ldg(reinterpret_cast<const double2*>(a.in) + base_a + j);
+          else v = make_double2(__ldg(&a.in[base_a + j]), vb ? __ldg(&a.in[base_a + N + j]) : 0.0);
+          v = cmul(v, __ldg(&T.chirp[j]));
           if (half) v = cmul(v, wM(j, octM, logM));
         }
         buf[swz(j)] = v;
@@ -299,7 +318,17 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
     double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
     for (int mi = threadIdx.x; mi < a.n_bins; mi += SPLIT_T) {
       const double2 y = cadd(u[mi], cmulc(buf[swz(mi)], wM(mi, octM, logM)));
-      out[(size_t)mi * a.n_rings + t] = cscale(cmul(__ldg(&T.chirp[mi]), y), a.scale);
+      const double2 z = cmul(__ldg(&T.chirp[mi]), y);
+      if (!a.real) {
+        out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+      } else {
+        const int mr = mi ? N - mi : 0;
+        const double2 yr = cadd(u[mr], cmulc(buf[swz(mr)], wM(mr, octM, logM)));
+        const double2 zr = cconj(cmul(__ldg(&T.chirp[mr]), yr));
+        const double h = 0.5 * a.scale;
+        out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
+        if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      }
     }
     __syncthreads();
   }
@@ -315,22 +344,33 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
   load_octant(octF, T.oct, logF);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
-  const int n_rows = a.n_sets * a.n_rings;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int n_rows = a.n_sets * per;
+  const int pole_ring = (T.N + 1) / 2 - 1 - a.t_offset;
   __syncthreads();
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
-    const int set = row / a.n_rings, t = row - set * a.n_rings;
-    const double2* G = a.in + ((size_t)set * a.n_rings + t) * a.n_bins;
+    const int set = row / per, p = row - set * per;
+    const int ta = a.real ? 2 * p : p;
+    const bool vb = a.real && ta + 1 < a.n_rings;
+    const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * a.n_bins;
+    const double2* Gb = Ga + a.n_bins;
     split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (n < N) {
           if (!a.real) {
-            v = __ldg(&G[n]);
-          } else if (n < a.n_bins) {
-            v = __ldg(&G[n]);
-            if (n == 0) v.y = 0.0;
+            v = __ldg(&Ga[n]);
           } else {
-            v = cconj(__ldg(&G[N - n]));
+            double2 X, Y = make_double2(0.0, 0.0);
+            if (n < a.n_bins) {
+              X = __ldg(&Ga[n]);
+              if (vb) Y = __ldg(&Gb[n]);
+              if (n == 0) X.y = Y.y = 0.0;
+            } else {
+              X = cconj(__ldg(&Ga[N - n]));
+              if (vb) Y = cconj(__ldg(&Gb[N - n]));
+            }
+            v = cadd(X, cmul_pi(Y));
           }
           v = cmulc(v, __ldg(&T.chirp[n]));
           if (half) v = cmul(v, wM(n, octM, logM));
@@ -338,14 +378,19 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
         buf[swz(n)] = v;
       }
     });
-    const bool pole = a.mw_pole && t + a.t_offset == (T.N + 1) / 2 - 1;
-    const double2 pv = pole ? __ldg(&G[0]) : make_double2(0.0, 0.0);
-    const size_t ob = ((size_t)set * a.n_rings + t) * N;
-    for (int p = threadIdx.x; p < N; p += SPLIT_T) {
-      const double2 y = cadd(u[p], cmulc(buf[swz(p)], wM(p, octM, logM)));
-      const double2 v = pole ? pv : cmulc(y, __ldg(&T.chirp[p]));
-      if (a.real) a.out[ob + p] = v.x;
-      else reinterpret_cast<double2*>(a.out)[ob + p] = v;
+    const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
+    const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
+    const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
+    const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+    for (int q = threadIdx.x; q < N; q += SPLIT_T) {
+      const double2 y = cadd(u[q], cmulc(buf[swz(q)], wM(q, octM, logM)));
+      const double2 v = cmulc(y, __ldg(&T.chirp[q]));
+      if (a.real) {
+        a.out[ob + q] = pa ? pva.x : v.x;
+        if (vb) a.out[ob + N + q] = pb ? pvb.x : v.y;
+      } else {
+        reinterpret_cast<double2*>(a.out)[ob + q] = pa ? pva : v;
+      }
     }
     __syncthreads();
   }
@@ -482,7 +527,7 @@ size_t fft_split_scratch_elems(int logM) {
 }
 
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
-  const int n_rows = a.n_sets * a.n_rings;
+  const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
   if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_fwd_split_kernel, a, n_rows, st);
   size_t smem;
@@ -495,7 +540,7 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
 }
 
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
-  const int n_rows = a.n_sets * a.n_rings;
+  const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
   if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_inv_split_kernel, a, n_rows, st);
   size_t smem;
