@@ -312,6 +312,21 @@ struct GridRes {
   double2 *oct = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
   double* seed_c = nullptr;
+  // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
+  int2 *pairs_r = nullptr, *pairs_c = nullptr;
+  int np_r = 0, np_c = 0;
+  double2* pole_resp = nullptr;
+
+  ThetaArgs theta(bool cplx) const {
+    ThetaArgs t;
+    t.T = fft();
+    t.k = k;
+    t.n_bins = n_bins(cplx);
+    t.pairs = cplx ? pairs_c : pairs_r;
+    t.n_pairs = cplx ? np_c : np_r;
+    t.pole_resp = pole_resp;
+    return t;
+  }
 
   FftTablesDev fft() const {
     FftTablesDev t;
@@ -354,6 +369,43 @@ template <class T>
 static int upload_new(T** dst, const std::vector<T>& v) {
   CU(cudaMalloc(dst, std::max<size_t>(16, v.size() * sizeof(T))));
   if (!v.empty()) CU(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return S2W_OK;
+}
+
+// Parity pairs for the theta stage and its response to a unit pole sample
+// (one even-row transform of e_{k-1}, run once per grid).
+static int theta_setup(GridRes* g) {
+  const int k = g->k;
+  std::vector<int2> pr;
+  theta_pairs(nullptr, k, k, pr);
+  g->np_r = (int)pr.size();
+  CHECK(upload_new(&g->pairs_r, pr));
+  theta_pairs(nullptr, g->N, k, pr);
+  g->np_c = (int)pr.size();
+  CHECK(upload_new(&g->pairs_c, pr));
+  std::vector<double2> imp(k, make_double2(0.0, 0.0));
+  imp[k - 1] = make_double2(1.0, 0.0);
+  double2 *d_imp = nullptr, *scratch = nullptr;
+  int2* one = nullptr;
+  CHECK(upload_new(&d_imp, imp));
+  CHECK(upload_new(&one, std::vector<int2>{make_int2(0, -1)}));
+  CU(cudaMalloc(&g->pole_resp, sizeof(double2) * k));
+  const size_t se = fft_split_scratch_elems(g->logM);
+  if (se) CU(cudaMalloc(&scratch, sizeof(double2) * se));
+  ThetaArgs ta = g->theta(false);
+  ta.n_sets = 1;
+  ta.n_bins = 1;
+  ta.pairs = one;
+  ta.n_pairs = 1;
+  ta.pole_resp = nullptr;
+  ta.in = d_imp;
+  ta.out = g->pole_resp;
+  ta.scratch = scratch;
+  CU(launch_theta(ta, 0));
+  CU(cudaStreamSynchronize(0));
+  cudaFree(d_imp);
+  cudaFree(one);
+  if (scratch) cudaFree(scratch);
   return S2W_OK;
 }
 
@@ -448,6 +500,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->wconv, spectrum_brev(w)));
   CHECK(upload_new(&g->ph1, ph1));
   CHECK(upload_new(&g->ph2, ph2));
+  if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   g_grids[key] = g;
   *out = g;
   return S2W_OK;
@@ -647,12 +700,8 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
     CU(launch_phi_fwd(pa, st));
   }
   if (g->scheme == S2W_SCHEME_MW) {
-    ThetaArgs ta;
-    ta.T = g->fft();
+    ThetaArgs ta = g->theta(!real);
     ta.n_sets = n_sets;
-    ta.k = g->k;
-    ta.n_bins = g->n_bins(!real);
-    ta.row_bin = nullptr;
     ta.in = G;
     ta.out = G;
     ta.scratch = scratch;
@@ -1165,12 +1214,8 @@ int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta
     CU(launch_phi_fwd(pa, (cudaStream_t)stream));
   }
   if (theta_stage) {
-    ThetaArgs ta;
-    ta.T = g->fft();
+    ThetaArgs ta = g->theta(!is_real);
     ta.n_sets = n_sets;
-    ta.k = g->k;
-    ta.n_bins = g->n_bins(!is_real);
-    ta.row_bin = nullptr;
     ta.in = (double2*)G;
     ta.out = (double2*)G;
     ta.scratch = g_test_scratch.as<double2>();

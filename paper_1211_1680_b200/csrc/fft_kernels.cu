@@ -14,6 +14,8 @@
 //
 // All odd-length DFTs (N = 2L-1) are Bluestein chirp-z transforms over the
 // power-of-two shared-memory FFT in fft.cuh.
+#include <algorithm>
+
 #include "fft.cuh"
 #include "s2w_internal.h"
 
@@ -157,6 +159,56 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
 }
 
 // ---------------------------------------------------------------- MW theta stage
+// Parity pairing: the operator (extension -> band-limited |sin| product ->
+// first k rings) commutes with the reflection R: n -> N-1-n.  An even-m row
+// x is extended evenly, an odd-m row y oddly, except at the pole sample n=k-1
+// (its own mirror) where both keep their value.  So z = x~ + y~ is transformed
+// once and split: with delta = y(k-1) and r = response to a unit pole sample
+// (even), the even part of the result is H_x + delta r and the odd part is
+// H_y - delta r.
+struct ThetaPair {
+  const double2* ge;  // even-m input row (nullptr: none)
+  const double2* go;  // odd-m input row
+  double2* he;
+  double2* ho;
+  double2 delta;      // odd row's pole sample
+};
+
+S2W_DEV ThetaPair theta_pair(const ThetaArgs& a, int row, bool valid) {
+  ThetaPair P{nullptr, nullptr, nullptr, nullptr, make_double2(0.0, 0.0)};
+  if (!valid) return P;
+  const int set = row / a.n_pairs, pi = row - set * a.n_pairs;
+  const int2 pr = a.pairs[pi];
+  const size_t base = (size_t)set * a.n_bins;
+  if (pr.x >= 0) {
+    P.ge = a.in + (base + pr.x) * a.k;
+    P.he = a.out + (base + pr.x) * a.k;
+  }
+  if (pr.y >= 0) {
+    P.go = a.in + (base + pr.y) * a.k;
+    P.ho = a.out + (base + pr.y) * a.k;
+    P.delta = __ldg(&P.go[a.k - 1]);
+  }
+  return P;
+}
+
+// extended sample n < N of the paired row
+S2W_DEV double2 theta_ext(const ThetaPair& P, int n, int k) {
+  const bool lo = n < k;
+  const int src = lo ? n : 2 * k - 2 - n;
+  const double2 e = P.ge ? __ldg(&P.ge[src]) : make_double2(0.0, 0.0);
+  const double2 o = P.go ? __ldg(&P.go[src]) : make_double2(0.0, 0.0);
+  return lo ? cadd(e, o) : csub(e, o);
+}
+
+// write ring t < k from w_t = result(t), w_r = result(N-1-t)
+S2W_DEV void theta_store(const ThetaPair& P, const ThetaArgs& a, int t, double2 wt, double2 wr) {
+  const double2 r = a.pole_resp ? __ldg(&a.pole_resp[t]) : make_double2(0.0, 0.0);
+  const double2 dr = cmul(P.delta, r);
+  if (P.he) P.he[t] = csub(cscale(cadd(wt, wr), 0.5), dr);
+  if (P.ho) P.ho[t] = cadd(cscale(csub(wt, wr), 0.5), dr);
+}
+
 __global__ void theta_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
@@ -166,14 +218,8 @@ __global__ void theta_kernel(ThetaArgs a) {
   double2* oct = smem + (size_t)a.rpc * M;
   load_octant(oct, T.oct, T.logM);
   const int row = blockIdx.x * a.rpc + grp;
-  const int n_rows = a.n_sets * a.n_bins;
-  const bool valid = row < n_rows;
-  const int set = valid ? row / a.n_bins : 0;
-  const int mi = valid ? row - set * a.n_bins : 0;  // storage row
-  const int bin = a.row_bin ? a.row_bin[mi] : mi;
-  const int m = (bin < k) ? bin : bin - N;
-  const double sgn = (m & 1) ? -1.0 : 1.0;
-  const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
+  const bool valid = row < a.n_sets * a.n_pairs;
+  const ThetaPair P = theta_pair(a, row, valid);
 
   // 1. parity extension to the full circle, times the Bluestein chirp
   for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
@@ -182,8 +228,7 @@ __global__ void theta_kernel(ThetaArgs a) {
     for (int u = 0; u < 8; ++u) {
       const int n = n0 + u * a.gsize;
       const bool in = valid && n < N;
-      x[u] = in ? ((n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn))
-                : make_double2(0.0, 0.0);
+      x[u] = in ? theta_ext(P, n, k) : make_double2(0.0, 0.0);
       c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
@@ -237,25 +282,16 @@ __global__ void theta_kernel(ThetaArgs a) {
   __syncthreads();
   for (int n = N + gtid; n < M; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
-  // 6. inverse DFT_N (Bluestein), keep the first k rings
+  // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
   fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
   if (!valid) return;
-  double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
-  for (int t0 = gtid; t0 < k; t0 += 8 * a.gsize) {
-    double2 c[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u * a.gsize;
-      c[u] = (t < k) ? __ldg(&T.chirp[t]) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u * a.gsize;
-      if (t < k) H[t] = cmulc(buf[swz(t)], c[u]);
-    }
+  for (int t = gtid; t < k; t += a.gsize) {
+    const int tr = N - 1 - t;
+    const double2 wt = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
+    const double2 wr = cmulc(buf[swz(tr)], __ldg(&T.chirp[tr]));
+    theta_store(P, a, t, wt, wr);
   }
 }
-
 
 // =====================================================================
 // Split mode for M > 8192 (L > 2048): the length-M cyclic convolution is
@@ -400,7 +436,6 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
   const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N, k = a.k;
-  const int M = 1 << logM;
   double2* buf = smem;
   double2* octF = smem + F;
   double2* octM = octF + oct_alloc(logF);
@@ -408,21 +443,16 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;   // even-half results
   double2* sv = u + F;                                  // saved row (a_bin, then X_bin)
-  const int n_rows = a.n_sets * a.n_bins;
+  const int n_rows = a.n_sets * a.n_pairs;
   __syncthreads();
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
-    const int set = row / a.n_bins, mi = row - set * a.n_bins;
-    const int bin = a.row_bin ? a.row_bin[mi] : mi;
-    const int m = (bin < k) ? bin : bin - N;
-    const double sgn = (m & 1) ? -1.0 : 1.0;
-    const double2* G = a.in + ((size_t)set * a.n_bins + mi) * k;
+    const ThetaPair P = theta_pair(a, row, true);
     // 1-2. DFT_N of the parity extension (Bluestein)
     split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (n < N) {
-          v = (n < k) ? __ldg(&G[n]) : cscale(__ldg(&G[2 * k - 2 - n]), sgn);
-          v = cmul(v, __ldg(&T.chirp[n]));
+          v = cmul(theta_ext(P, n, k), __ldg(&T.chirp[n]));
           if (half) v = cmul(v, wM(n, octM, logM));
         }
         buf[swz(n)] = v;
@@ -461,7 +491,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
       sv[b] = cmul(h, __ldg(&T.ph2[b]));
     }
     __syncthreads();
-    // 6. inverse DFT_N (Bluestein), first k rings
+    // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
     split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = (n < N) ? sv[n] : make_double2(0.0, 0.0);
@@ -469,13 +499,13 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
         buf[swz(n)] = v;
       }
     });
-    double2* H = a.out + ((size_t)set * a.n_bins + mi) * k;
     for (int t = threadIdx.x; t < k; t += SPLIT_T) {
-      const double2 z = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
-      H[t] = cmulc(z, __ldg(&T.chirp[t]));
+      const int tr = N - 1 - t;
+      const double2 zt = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
+      const double2 zr = cadd(u[tr], cmulc(buf[swz(tr)], wM(tr, octM, logM)));
+      theta_store(P, a, t, cmulc(zt, __ldg(&T.chirp[t])), cmulc(zr, __ldg(&T.chirp[tr])));
     }
     __syncthreads();
-    (void)M;
   }
 }
 
@@ -552,8 +582,22 @@ cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
+  const int N = 2 * k - 1;
+  std::vector<int> ev, od;
+  for (int r = 0; r < n_rows; ++r) {
+    const int bin = bins ? bins[r] : r;
+    const int m = bin < k ? bin : bin - N;
+    ((m & 1) ? od : ev).push_back(r);
+  }
+  const size_t n = std::max(ev.size(), od.size());
+  pairs.resize(n);
+  for (size_t i = 0; i < n; ++i)
+    pairs[i] = make_int2(i < ev.size() ? ev[i] : -1, i < od.size() ? od[i] : -1);
+}
+
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
-  const int n_rows = a.n_sets * a.n_bins;
+  const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
   if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(theta_split_kernel, a, n_rows, st);
   size_t smem;

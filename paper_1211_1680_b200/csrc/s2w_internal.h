@@ -1,6 +1,7 @@
 // Internal (non-ABI) declarations shared by the s2w CUDA translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <vector>
 
 namespace s2w {
 
@@ -44,10 +45,15 @@ struct PhiInvArgs {
   double2* scratch;
 };
 
+// The theta operator commutes with the reflection theta -> 2 pi - theta, so an
+// even-m row (even extension) and an odd-m row (odd extension) are summed and
+// transformed together, then separated by parity (see theta_kernel).
 struct ThetaArgs {
   FftTablesDev T;
   int n_sets, k, n_bins;  // n_bins = rows per set
-  const int* row_bin;     // row -> azimuthal bin (order-sharded rows); nullptr = identity
+  const int2* pairs;      // [n_pairs] (even-m row, odd-m row) per transform, -1 = none
+  int n_pairs;
+  const double2* pole_resp;  // [k] response to a unit pole sample (nullptr: no odd rows)
   const double2* in;  // [set][mi][k]
   double2* out;       // [set][mi][k] (may alias in)
   int gsize, rpc;
@@ -59,6 +65,8 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
 size_t fft_split_scratch_elems(int logM);
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st);
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st);
+// Pair storage rows by the parity of their order m (bins[row] = azimuthal bin).
+void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs);
 
 // ------------------------------------------------------------------ Legendre
 struct LegGridDev {
