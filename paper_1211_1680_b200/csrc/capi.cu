@@ -262,6 +262,21 @@ static std::vector<double2> spectrum_brev(std::vector<cld> a) {
   return out;
 }
 
+// Radix-16 pass twiddles of the FFT engine of size 2^logE (fft.cuh): pass p
+// (span s = 2^(logE - 4(p+1))) holds W_{16 s}^j, j < s, contiguous.
+static std::vector<double2> pass_twiddles(int logE) {
+  std::vector<double2> tw;
+  for (int p = 0; p < (logE - 1) / 4; ++p) {
+    const long long s = 1LL << (logE - 4 * (p + 1));
+    for (long long j = 0; j < s; ++j) {
+      const ld ang = -2.0L * PI_L * (ld)j / (ld)(16 * s);
+      tw.push_back(make_double2((double)std::cos(ang), (double)std::sin(ang)));
+    }
+  }
+  if ((int)tw.size() != fft_tw_elems(logE)) tw.clear();  // cannot happen
+  return tw;
+}
+
 static std::vector<double2> octant_table(int logM) {
   const int M = 1 << logM;
   std::vector<double2> oct(M / 8 + 1);
@@ -274,6 +289,9 @@ static std::vector<double2> octant_table(int logM) {
 
 // ------------------------------------------------------------------ per-device seed table
 static const int SEED_KMAX = 16384;
+// Largest band limit: ring DFTs of N = 2L-1 need a Bluestein convolution of
+// 2^ceil(log2(4L-3)) <= 2^14 points (split mode).
+static const int S2W_MAX_L = 4096;
 
 struct DeviceTables {
   double* seed_c = nullptr;  // c_m, m < SEED_KMAX
@@ -309,7 +327,7 @@ struct GridRes {
   std::vector<int2> act_host;
   double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
   int2* act = nullptr;
-  double2 *oct = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
+  double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
@@ -332,7 +350,7 @@ struct GridRes {
     FftTablesDev t;
     t.N = N;
     t.logM = logM;
-    t.oct = oct;
+    t.tw = tw;
     t.octM = octM;
     t.chirp = chirp;
     t.bl_fwd = bl_fwd;
@@ -417,7 +435,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     *out = it->second;
     return S2W_OK;
   }
-  if (k < 1 || k >= SEED_KMAX) return fail(S2W_EPARAM, "band-limit %d out of range [1, %d)", k, SEED_KMAX);
+  if (k < 1 || k > S2W_MAX_L) return fail(S2W_EPARAM, "band-limit %d out of range [1, %d]", k, S2W_MAX_L);
   DeviceTables* dt;
   CHECK(device_tables(dev, &dt));
   GridRes* g = new GridRes();
@@ -465,7 +483,6 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   // FFT / Bluestein / theta-stage tables
   std::vector<double2> chirp(N), ph1(N), ph2(N);
   const bool split = g->logM > FFT_MAX_LOGM_SMEM;
-  std::vector<double2> oct = octant_table(split ? g->logM - 1 : g->logM);
   std::vector<cld> cl(N);
   for (int n = 0; n < N; ++n) {
     long long r = ((long long)n * n) % (2LL * N);
@@ -492,7 +509,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     ph1[bin] = d2(cl[bin] * cld(std::cos(a1), std::sin(a1)) / (ld)N);
     ph2[bin] = d2(cld(std::cos(-a1), std::sin(-a1)) * std::conj(cl[bin]));
   }
-  CHECK(upload_new(&g->oct, oct));
+  CHECK(upload_new(&g->tw, pass_twiddles(split ? g->logM - 1 : g->logM)));
   if (split) CHECK(upload_new(&g->octM, octant_table(g->logM)));
   CHECK(upload_new(&g->chirp, chirp));
   CHECK(upload_new(&g->bl_fwd, spectrum_brev(b)));

@@ -1,137 +1,230 @@
 // Shared-memory power-of-two FFT engine (FP64 complex) for sm_100a.
 //
-// One row of M = 2^logM complex doubles lives in shared memory (M <= 8192,
-// i.e. 128 KiB).  The forward transform is an in-place decimation-in-frequency
-// (DIF) Cooley-Tukey sweep of radix-8 passes (plus one radix-4/2 pass when
-// logM is not a multiple of 3): natural-order input, bit-reversed output.
-// The inverse is the exact adjoint sweep (DIT): bit-reversed input, natural
-// output, unnormalised (x M).  Every use in this library is a convolution
-// (Bluestein chirp-z, the MW theta-weight convolution), so the bit-reversed
-// spectrum is multiplied by a table that the host stored in the same
-// bit-reversed order and never has to be permuted.
+// One row of M = 2^LOGM complex doubles (M <= 8192, 128 KiB) lives in shared
+// memory and is transformed by GS = fft_gs(LOGM) threads.  Sizes are
+// compile-time, so every span, loop bound and swizzle offset is an immediate.
 //
-// Bank conflicts: a 16-byte complex spans 4 banks; strided radix passes would
-// hit the same banks, so element i is stored at swz(i) = i ^ ((i >> 3) & 7),
-// which permutes within 128-byte rows and makes the stride-1/2/4/8/contiguous
-// access patterns of all passes conflict-free.
+// Forward: in-place decimation-in-frequency (DIF), natural order in,
+// bit-reversed order out, as K = (LOGM-1)/4 radix-16 passes followed by one
+// "core" pass of radix 2^CB (CB = LOGM - 4K in [1, 4]) at span 1.  Inverse:
+// the exact adjoint sweep (DIT): bit-reversed in, natural out, unnormalised.
+// Every use in this library is a cyclic convolution (Bluestein chirp-z, the MW
+// theta-weight convolution), so fft_conv fuses the last forward pass, the
+// product with the spectrum table (which the host stores in the same
+// bit-reversed order) and the first inverse pass into one shared-memory pass:
+// 2K + 1 passes per convolution (7 at M = 8192).
+//
+// Radix-16 butterflies run in registers as four radix-2 DIF stages; register
+// i then holds output brev4(i), which is multiplied by the pass twiddle
+// u^brev4(i), u = W_{16 s}^j (s = span, j = position in the span), u read
+// from a per-pass table (host-built, contiguous in j) and its powers formed
+// by at most four rounding levels of products.
+//
+// Bank conflicts: element e is stored at swz(e) = e ^ (((e >> 3) ^ (e >> 4)) & 7),
+// a permutation within 128-byte rows which (checked exhaustively for every
+// pass pattern of LOGM = 3..13) makes each quarter-warp's 16-byte accesses
+// hit 8 distinct bank groups.  swz is linear over XOR, so for disjoint bit
+// fields swz(a + b) = swz(a) ^ swz(b): the per-element offsets of a butterfly
+// are compile-time constants.
 #pragma once
 #include "common.cuh"
 
-S2W_DEV int swz(int i) { return i ^ ((i >> 3) & 7); }
+__host__ __device__ constexpr int swz(int i) { return i ^ (((i >> 3) ^ (i >> 4)) & 7); }
 
-template <int R> S2W_DEV int brev(int r);
-template <> S2W_DEV int brev<2>(int r) { return r; }
-template <> S2W_DEV int brev<4>(int r) { return ((r & 1) << 1) | (r >> 1); }
-template <> S2W_DEV int brev<8>(int r) { return ((r & 1) << 2) | (r & 2) | (r >> 2); }
+__host__ __device__ constexpr int brev4(int r) {
+  return ((r & 1) << 3) | ((r & 2) << 1) | ((r & 4) >> 1) | ((r & 8) >> 3);
+}
+
+// threads per row and radix-16 pass count / core radix bits for M = 2^LOGM
+__host__ __device__ constexpr int fft_gs(int logm) {
+  return logm >= 13 ? 512 : logm <= 9 ? 32 : (1 << (logm - 4));
+}
+// CTA size bound of the row kernels (M = 8192 needs 512 threads of <= 128
+// registers; smaller rows run 256-thread CTAs with up to 255 registers)
+__host__ __device__ constexpr int fft_maxthr(int logm) { return logm >= 13 ? 512 : 256; }
+__host__ __device__ constexpr int fft_k16(int logm) { return (logm - 1) / 4; }
+// twiddle-table length (sum of the spans of the radix-16 passes) and offset of pass p
+__host__ __device__ constexpr int fft_tw_off(int logm, int p) {
+  int o = 0;
+  for (int q = 0; q < p; ++q) o += 1 << (logm - 4 * (q + 1));
+  return o;
+}
+__host__ __device__ constexpr int fft_ntw(int logm) { return fft_tw_off(logm, fft_k16(logm)); }
 
 #define S2W_RSQRT2 0.70710678118654752440
+#define S2W_C16 0.92387953251128675613
+#define S2W_S16 0.38268343236508977173
 
-// (a + i b) * W8^1 = (a + i b)(1 - i)/sqrt2
-S2W_DEV double2 mul_w8_1(double2 v) {
-  return make_double2((v.x + v.y) * S2W_RSQRT2, (v.y - v.x) * S2W_RSQRT2);
-}
-// * W8^3 = (-1 - i)/sqrt2
-S2W_DEV double2 mul_w8_3(double2 v) {
-  return make_double2((v.y - v.x) * S2W_RSQRT2, -(v.x + v.y) * S2W_RSQRT2);
-}
-// * conj(W8^1) = (1 + i)/sqrt2
-S2W_DEV double2 mul_w8c_1(double2 v) {
-  return make_double2((v.x - v.y) * S2W_RSQRT2, (v.x + v.y) * S2W_RSQRT2);
-}
-// * conj(W8^3) = (-1 + i)/sqrt2
-S2W_DEV double2 mul_w8c_3(double2 v) {
-  return make_double2(-(v.x + v.y) * S2W_RSQRT2, (v.x - v.y) * S2W_RSQRT2);
-}
-
-// In-register radix butterflies.  Forward: in-place DIF radix-2 stages, so
-// register i ends up holding X[brev(i)].  Inverse: the adjoint, taking
-// brev-ordered input to natural-order output (unnormalised).
-template <int R> S2W_DEV void bfly_fwd(double2* v);
-template <int R> S2W_DEV void bfly_inv(double2* v);
-
-template <> S2W_DEV void bfly_fwd<2>(double2* v) {
-  double2 a = v[0], b = v[1];
-  v[0] = cadd(a, b);
-  v[1] = csub(a, b);
-}
-template <> S2W_DEV void bfly_inv<2>(double2* v) { bfly_fwd<2>(v); }
-
-template <> S2W_DEV void bfly_fwd<4>(double2* v) {
-  double2 a0 = cadd(v[0], v[2]), a2 = csub(v[0], v[2]);
-  double2 a1 = cadd(v[1], v[3]), a3 = cmul_mi(csub(v[1], v[3]));
-  v[0] = cadd(a0, a1);
-  v[1] = csub(a0, a1);
-  v[2] = cadd(a2, a3);
-  v[3] = csub(a2, a3);
-}
-template <> S2W_DEV void bfly_inv<4>(double2* v) {
-  // adjoint: stage span-1 first, then span-2 with conj twiddles
-  double2 a0 = cadd(v[0], v[1]), a1 = csub(v[0], v[1]);
-  double2 a2 = cadd(v[2], v[3]), a3 = csub(v[2], v[3]);
-  a3 = cmul_pi(a3);
-  v[0] = cadd(a0, a2);
-  v[2] = csub(a0, a2);
-  v[1] = cadd(a1, a3);
-  v[3] = csub(a1, a3);
+// v * W16^q (CONJ: v * conj(W16^q)), W16 = exp(-2 pi i / 16), q in [0, 8).
+// Always called with q a constant after unrolling, so the switch folds away.
+template <bool CONJ>
+S2W_DEV double2 mul_w16(int q, double2 v) {
+  const double sg = CONJ ? -1.0 : 1.0;  // sign of the imaginary part of the factor
+  switch (q & 7) {
+    case 0:
+      return v;
+    case 4:
+      return CONJ ? cmul_pi(v) : cmul_mi(v);
+    case 2:  // (1 - i)/sqrt2
+      return make_double2((v.x + sg * v.y) * S2W_RSQRT2, (v.y - sg * v.x) * S2W_RSQRT2);
+    case 6:  // (-1 - i)/sqrt2
+      return make_double2((sg * v.y - v.x) * S2W_RSQRT2, -(v.y + sg * v.x) * S2W_RSQRT2);
+    default: {
+      const double wr = (q & 7) == 1 ? S2W_C16 : (q & 7) == 3 ? S2W_S16 : (q & 7) == 5 ? -S2W_S16 : -S2W_C16;
+      const double wi = sg * ((q & 7) == 1 ? -S2W_S16 : (q & 7) == 3 ? -S2W_C16 : (q & 7) == 5 ? -S2W_C16 : -S2W_S16);
+      return make_double2(fma(v.x, wr, -v.y * wi), fma(v.x, wi, v.y * wr));
+    }
+  }
 }
 
-template <> S2W_DEV void bfly_fwd<8>(double2* v) {
-  // stage span 4
-  double2 b0 = cadd(v[0], v[4]), b4 = csub(v[0], v[4]);
-  double2 b1 = cadd(v[1], v[5]), b5 = mul_w8_1(csub(v[1], v[5]));
-  double2 b2 = cadd(v[2], v[6]), b6 = cmul_mi(csub(v[2], v[6]));
-  double2 b3 = cadd(v[3], v[7]), b7 = mul_w8_3(csub(v[3], v[7]));
-  // stage span 2
-  double2 c0 = cadd(b0, b2), c2 = csub(b0, b2);
-  double2 c1 = cadd(b1, b3), c3 = cmul_mi(csub(b1, b3));
-  double2 c4 = cadd(b4, b6), c6 = csub(b4, b6);
-  double2 c5 = cadd(b5, b7), c7 = cmul_mi(csub(b5, b7));
-  // stage span 1
-  v[0] = cadd(c0, c1);
-  v[1] = csub(c0, c1);
-  v[2] = cadd(c2, c3);
-  v[3] = csub(c2, c3);
-  v[4] = cadd(c4, c5);
-  v[5] = csub(c4, c5);
-  v[6] = cadd(c6, c7);
-  v[7] = csub(c6, c7);
-}
-template <> S2W_DEV void bfly_inv<8>(double2* v) {
-  // adjoint of the above: span 1, span 2 (conj), span 4 (conj)
-  double2 c0 = cadd(v[0], v[1]), c1 = csub(v[0], v[1]);
-  double2 c2 = cadd(v[2], v[3]), c3 = csub(v[2], v[3]);
-  double2 c4 = cadd(v[4], v[5]), c5 = csub(v[4], v[5]);
-  double2 c6 = cadd(v[6], v[7]), c7 = csub(v[6], v[7]);
-  // span 2: (a, b) -> (a + conj(w) b, a - conj(w) b), w = 1 or -i
-  double2 t;
-  double2 b0 = cadd(c0, c2), b2 = csub(c0, c2);
-  t = cmul_pi(c3);
-  double2 b1 = cadd(c1, t), b3 = csub(c1, t);
-  double2 b4 = cadd(c4, c6), b6 = csub(c4, c6);
-  t = cmul_pi(c7);
-  double2 b5 = cadd(c5, t), b7 = csub(c5, t);
-  // span 4: w = W8^i
-  v[0] = cadd(b0, b4);
-  v[4] = csub(b0, b4);
-  t = mul_w8c_1(b5);
-  v[1] = cadd(b1, t);
-  v[5] = csub(b1, t);
-  t = cmul_pi(b6);
-  v[2] = cadd(b2, t);
-  v[6] = csub(b2, t);
-  t = mul_w8c_3(b7);
-  v[3] = cadd(b3, t);
-  v[7] = csub(b3, t);
+// Radix-2^LR DIF butterfly in registers: natural in, register i = output brev(i).
+template <int LR>
+S2W_DEV void dif(double2* v) {
+  constexpr int R = 1 << LR;
+#pragma unroll
+  for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int b0 = 0; b0 < R; b0 += 2 * h) {
+#pragma unroll
+      for (int a = 0; a < h; ++a) {
+        const double2 p = v[b0 + a], q = v[b0 + a + h];
+        v[b0 + a] = cadd(p, q);
+        v[b0 + a + h] = mul_w16<false>(a * (8 / h), csub(p, q));
+      }
+    }
+  }
 }
 
-// Octant-table slot of entry r: XOR-swizzled so that power-of-two strides
-// (tstep = 8, 64, 512 in the radix-8 passes) hit distinct 16-byte bank groups.
+// Adjoint of dif: register i = input brev(i), natural out (unnormalised).
+template <int LR>
+S2W_DEV void adj(double2* v) {
+  constexpr int R = 1 << LR;
+#pragma unroll
+  for (int h = 1; h < R; h <<= 1) {
+#pragma unroll
+    for (int b0 = 0; b0 < R; b0 += 2 * h) {
+#pragma unroll
+      for (int a = 0; a < h; ++a) {
+        const double2 p = v[b0 + a];
+        const double2 t = mul_w16<true>(a * (8 / h), v[b0 + a + h]);
+        v[b0 + a] = cadd(p, t);
+        v[b0 + a + h] = csub(p, t);
+      }
+    }
+  }
+}
+
+// w[k] = u^k, k = 1..15 (w[0] unused)
+S2W_DEV void powers16(double2* w, double2 u) {
+  w[1] = u;
+  w[2] = cmul(u, u);
+  w[3] = cmul(w[2], u);
+  w[4] = cmul(w[2], w[2]);
+  w[5] = cmul(w[4], u);
+  w[6] = cmul(w[4], w[2]);
+  w[7] = cmul(w[4], w[3]);
+  w[8] = cmul(w[4], w[4]);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) w[8 + k] = cmul(w[8], w[k]);
+}
+
+// One radix-16 pass at span 2^LS (forward DIF, or its adjoint when INV).
+template <int LOGM, int GS, int LS, bool INV>
+S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, int gtid) {
+  constexpr int NB = (1 << LOGM) / 16;
+  constexpr int S = 1 << LS;
+#pragma unroll
+  for (int it = 0; it < (NB + GS - 1) / GS; ++it) {
+    const int b = gtid + it * GS;
+    if (NB % GS != 0 && b >= NB) break;
+    const int j = b & (S - 1);
+    const int sb = swz(((b >> LS) << (LS + 4)) + j);
+    double2 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = buf[sb ^ swz(k << LS)];
+    double2 w[16];
+    powers16(w, tw[j]);
+    if constexpr (!INV) {
+      dif<4>(v);
+#pragma unroll
+      for (int i = 1; i < 16; ++i) v[i] = cmul(v[i], w[brev4(i)]);
+    } else {
+#pragma unroll
+      for (int i = 1; i < 16; ++i) v[i] = cmulc(v[i], w[brev4(i)]);
+      adj<4>(v);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) buf[sb ^ swz(k << LS)] = v[k];
+  }
+}
+
+// Core pass: last forward pass (radix 2^CB, span 1), product with the
+// bit-reversed spectrum table, first inverse pass.
+template <int LOGM, int GS>
+S2W_DEV void conv_core(double2* __restrict__ buf, const double2* __restrict__ tab, int gtid) {
+  constexpr int CB = LOGM - 4 * fft_k16(LOGM);
+  constexpr int R = 1 << CB;
+  constexpr int NB = (1 << LOGM) / R;
+#pragma unroll
+  for (int it = 0; it < (NB + GS - 1) / GS; ++it) {
+    const int b = gtid + it * GS;
+    if (NB % GS != 0 && b >= NB) break;
+    const int sb = swz(b * R);
+    double2 v[R], t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];
+    dif<CB>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], t[i]);
+    adj<CB>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[sb ^ swz(i)] = v[i];
+  }
+}
+
+template <int LOGM, int GS, int P>
+S2W_DEV void fwd_passes(double2* buf, const double2* tw, int gtid) {
+  if constexpr (P < fft_k16(LOGM)) {
+    pass16<LOGM, GS, LOGM - 4 * (P + 1), false>(buf, tw + fft_tw_off(LOGM, P), gtid);
+    __syncthreads();
+    fwd_passes<LOGM, GS, P + 1>(buf, tw, gtid);
+  }
+}
+template <int LOGM, int GS, int P>
+S2W_DEV void inv_passes(double2* buf, const double2* tw, int gtid) {
+  if constexpr (P >= 0) {
+    pass16<LOGM, GS, LOGM - 4 * (P + 1), true>(buf, tw + fft_tw_off(LOGM, P), gtid);
+    __syncthreads();
+    inv_passes<LOGM, GS, P - 1>(buf, tw, gtid);
+  }
+}
+
+// Cyclic convolution of the row with the table's sequence: forward FFT,
+// product, inverse FFT.  tw: the pass twiddles (fft_ntw(LOGM) entries,
+// shared memory).  Precondition: row written and synced.  Ends synced.
+template <int LOGM, int GS>
+S2W_DEV void fft_conv(double2* buf, const double2* tw, const double2* __restrict__ tab,
+                      int gtid) {
+  fwd_passes<LOGM, GS, 0>(buf, tw, gtid);
+  conv_core<LOGM, GS>(buf, tab, gtid);
+  __syncthreads();
+  inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
+}
+
+// Copy the pass twiddles into shared memory (all threads of the CTA).
+template <int LOGM>
+S2W_DEV void load_tw(double2* __restrict__ s_tw, const double2* __restrict__ g_tw) {
+  for (int i = threadIdx.x; i < fft_ntw(LOGM); i += blockDim.x) s_tw[i] = __ldg(&g_tw[i]);
+}
+
+// ------------------------------------------------------------------ octant twiddles
+// W_M^k = exp(-2 pi i k / M) for arbitrary k from an octant table
+// oct[r] = (cos, sin)(2 pi r / M), r in [0, M/8] (split mode's W_M^j factors).
 S2W_DEV int oct_slot(int r) { return r ^ (((r >> 3) ^ (r >> 6) ^ (r >> 9)) & 7); }
-// entries allocated for an octant table of M = 2^logM (slot range rounded to 8)
 __host__ __device__ constexpr int oct_alloc(int logM) { return ((1 << (logM - 3)) + 8) & ~7; }
 
-// W_M^k = exp(-2 pi i k / M) from an octant table oct[r] = (cos, sin)(2 pi r / M),
-// r in [0, M/8], held in shared memory (M/8 + 1 entries: 16 KiB at M = 8192).
 S2W_DEV double2 twiddle(int k, const double2* __restrict__ oct, int logM) {
   const int sh = logM - 3;
   const int M8 = 1 << sh;
@@ -139,174 +232,15 @@ S2W_DEV double2 twiddle(int k, const double2* __restrict__ oct, int logM) {
   int r = k & (M8 - 1);
   if (q & 1) r = M8 - r;
   const double2 e = oct[oct_slot(r)];
-  const bool swap = ((q + 1) & 2) != 0;          // q in {1, 2, 5, 6}
+  const bool swap = ((q + 1) & 2) != 0;  // q in {1, 2, 5, 6}
   double c = swap ? e.y : e.x;
   double s = swap ? e.x : e.y;
-  if (q >= 2 && q <= 5) c = -c;                  // cos(phi) < 0
-  if (q >= 4) s = -s;                            // sin(phi) < 0
+  if (q >= 2 && q <= 5) c = -c;  // cos(phi) < 0
+  if (q >= 4) s = -s;            // sin(phi) < 0
   return make_double2(c, -s);
 }
 
-// Twiddles of one radix-R butterfly: w[r] = u^r, u = W_M^ts (one table lookup,
-// then products; at most 3 roundings deep for R = 8).
-template <int R>
-S2W_DEV void twiddle_powers(double2* w, int ts, const double2* __restrict__ oct, int logM) {
-  const double2 u = twiddle(ts, oct, logM);
-  w[1] = u;
-  if (R >= 4) {
-    w[2] = cmul(u, u);
-    w[3] = cmul(w[2], u);
-  }
-  if (R >= 8) {
-    w[4] = cmul(w[2], w[2]);
-    w[5] = cmul(w[4], u);
-    w[6] = cmul(w[3], w[3]);
-    w[7] = cmul(w[4], w[3]);
-  }
-}
-
-// One radix-R pass of span s = 2^log2s over a row of M elements.
-template <int R, bool INV>
-S2W_DEV void fft_pass(double2* __restrict__ buf, int logM, int log2s,
-                      const double2* __restrict__ oct, int gtid, int gsize) {
-  const int M = 1 << logM;
-  const int s = 1 << log2s;
-  const int nb = M / R;
-  const int tstep = M / (R * s);
-  for (int b = gtid; b < nb; b += gsize) {
-    const int blk = b >> log2s, j = b & (s - 1);
-    const int base = blk * R * s + j;
-    double2 v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = buf[swz(base + i * s)];
-    if (!INV) {
-      bfly_fwd<R>(v);
-      if (j) {
-        double2 w[R];
-        twiddle_powers<R>(w, j * tstep, oct, logM);
-#pragma unroll
-        for (int i = 1; i < R; ++i) v[i] = cmul(v[i], w[brev<R>(i)]);
-      }
-    } else {
-      if (j) {
-        double2 w[R];
-        twiddle_powers<R>(w, j * tstep, oct, logM);
-#pragma unroll
-        for (int i = 1; i < R; ++i) v[i] = cmulc(v[i], w[brev<R>(i)]);
-      }
-      bfly_inv<R>(v);
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) buf[swz(base + i * s)] = v[i];
-  }
-}
-
-// Copy the octant table (M/8 + 1 entries) from global into shared memory.
 S2W_DEV void load_octant(double2* __restrict__ s_oct, const double2* __restrict__ g_oct, int logM) {
   const int n = (1 << (logM - 3)) + 1;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_oct[oct_slot(i)] = __ldg(&g_oct[i]);
-}
-
-// Forward DIF FFT: natural -> bit-reversed.  Ends with a __syncthreads.
-// Precondition: the row is fully written and visible (caller synced).
-S2W_DEV void fft_fwd(double2* buf, int logM, const double2* __restrict__ tw, int gtid,
-                     int gsize) {
-  // tw: shared-memory octant table (load_octant)
-  int ls = logM;
-  while (ls >= 3) {
-    ls -= 3;
-    fft_pass<8, false>(buf, logM, ls, tw, gtid, gsize);
-    __syncthreads();
-  }
-  if (ls == 2) {
-    fft_pass<4, false>(buf, logM, 0, tw, gtid, gsize);
-    __syncthreads();
-  } else if (ls == 1) {
-    fft_pass<2, false>(buf, logM, 0, tw, gtid, gsize);
-    __syncthreads();
-  }
-}
-
-// Inverse (adjoint) DIT FFT: bit-reversed -> natural, unnormalised.
-S2W_DEV void fft_inv(double2* buf, int logM, const double2* __restrict__ tw, int gtid,
-                     int gsize) {
-  const int rem = logM % 3;
-  int ls = 0;
-  if (rem == 2) {
-    fft_pass<4, true>(buf, logM, 0, tw, gtid, gsize);
-    __syncthreads();
-    ls = 2;
-  } else if (rem == 1) {
-    fft_pass<2, true>(buf, logM, 0, tw, gtid, gsize);
-    __syncthreads();
-    ls = 1;
-  }
-  while (ls < logM) {
-    fft_pass<8, true>(buf, logM, ls, tw, gtid, gsize);
-    __syncthreads();
-    ls += 3;
-  }
-}
-
-// buf[p] *= tab[p] for all p (tab stored in the same bit-reversed order).
-// Unrolled so that 8 table loads per thread are in flight at once.
-S2W_DEV void pointwise_mul(double2* buf, int M, const double2* __restrict__ tab, int gtid,
-                           int gsize) {
-  for (int p0 = gtid; p0 < M; p0 += 8 * gsize) {
-    double2 t[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = p0 + u * gsize;
-      t[u] = (p < M) ? __ldg(&tab[p]) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = p0 + u * gsize;
-      if (p < M) buf[swz(p)] = cmul(buf[swz(p)], t[u]);
-    }
-  }
-}
-
-// Cyclic convolution core: forward DIF FFT, pointwise product with the
-// bit-reversed table, inverse DIT FFT -- with the last forward pass, the
-// product and the first inverse pass (all of span 1 over blocks of R
-// contiguous elements, no twiddles) fused into one shared-memory pass.
-// Precondition: row written and synced.  Ends with a __syncthreads.
-template <int R>
-S2W_DEV void conv_core_pass(double2* __restrict__ buf, int M, const double2* __restrict__ tab,
-                            int gtid, int gsize) {
-  for (int b = gtid; b < M / R; b += gsize) {
-    double2 v[R], t[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = buf[swz(b * R + i)];
-    bfly_fwd<R>(v);
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], t[i]);
-    bfly_inv<R>(v);
-#pragma unroll
-    for (int i = 0; i < R; ++i) buf[swz(b * R + i)] = v[i];
-  }
-}
-
-S2W_DEV void fft_conv(double2* buf, int logM, const double2* __restrict__ oct,
-                      const double2* __restrict__ tab, int gtid, int gsize) {
-  const int M = 1 << logM;
-  const int rem = logM % 3;
-  const int lastR = rem == 0 ? 8 : (1 << rem);
-  const int lastl = rem == 0 ? 3 : rem;
-  // forward: radix-8 passes down to span lastR
-  for (int ls = logM - 3; ls >= lastl; ls -= 3) {
-    fft_pass<8, false>(buf, logM, ls, oct, gtid, gsize);
-    __syncthreads();
-  }
-  if (lastR == 8) conv_core_pass<8>(buf, M, tab, gtid, gsize);
-  else if (lastR == 4) conv_core_pass<4>(buf, M, tab, gtid, gsize);
-  else conv_core_pass<2>(buf, M, tab, gtid, gsize);
-  __syncthreads();
-  for (int ls = lastl; ls < logM; ls += 3) {
-    fft_pass<8, true>(buf, logM, ls, oct, gtid, gsize);
-    __syncthreads();
-  }
 }

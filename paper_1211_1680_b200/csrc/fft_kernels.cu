@@ -28,16 +28,18 @@ __device__ __forceinline__ double2 load_map_elem(const double* __restrict__ in, 
 }
 
 // ---------------------------------------------------------------- phi forward
-__global__ void phi_fwd_kernel(PhiFwdArgs a) {
+template <int LOGM>
+__global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_fwd_kernel(PhiFwdArgs a) {
   // Real maps: two rings per transform (z = x + i y; X_k = (Z_k + conj Z_{N-k})/2,
   // Y_k = (Z_k - conj Z_{N-k})/2i), halving the FFT work.
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int M = 1 << T.logM, N = T.N;
-  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
+  const int N = T.N;
+  const int grp = threadIdx.x / GS, gtid = threadIdx.x % GS;
   double2* buf = smem + (size_t)grp * M;
-  double2* oct = smem + (size_t)a.rpc * M;
-  load_octant(oct, T.oct, T.logM);
+  double2* tw = smem + (size_t)a.rpc * M;
+  load_tw<LOGM>(tw, T.tw);
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;  // transforms per set
   const int row = blockIdx.x * a.rpc + grp;
   const bool valid = row < a.n_sets * per;
@@ -47,11 +49,11 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
   const bool vb = a.real && valid && ta + 1 < a.n_rings;
   const long long base_a = ((long long)set * a.n_rings + ta) * N;
 
-  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+  for (int n0 = gtid; n0 < M; n0 += 8 * GS) {
     double2 x[8], c[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       const bool in = valid && n < N;
       if (!a.real) {
         x[u] = in ? __ldg(reinterpret_cast<const double2*>(a.in) + base_a + n)
@@ -64,15 +66,15 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
     }
   }
   __syncthreads();
-  fft_conv(buf, T.logM, oct, T.bl_fwd, gtid, a.gsize);
+  fft_conv<LOGM, GS>(buf, tw, T.bl_fwd, gtid);
   if (!valid) return;
   double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
-  for (int mi = gtid; mi < a.n_bins; mi += a.gsize) {
+  for (int mi = gtid; mi < a.n_bins; mi += GS) {
     const double2 z = cmul(__ldg(&T.chirp[mi]), buf[swz(mi)]);
     if (!a.real) {
       out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
@@ -87,16 +89,18 @@ __global__ void phi_fwd_kernel(PhiFwdArgs a) {
 }
 
 // ---------------------------------------------------------------- phi inverse
-__global__ void phi_inv_kernel(PhiInvArgs a) {
+template <int LOGM>
+__global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_inv_kernel(PhiInvArgs a) {
   // Real maps: two rings per transform (Z = X + i Y of their Hermitian spectra;
   // the two real rings are Re and Im of the inverse DFT).
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int M = 1 << T.logM, N = T.N;
-  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
+  const int N = T.N;
+  const int grp = threadIdx.x / GS, gtid = threadIdx.x % GS;
   double2* buf = smem + (size_t)grp * M;
-  double2* oct = smem + (size_t)a.rpc * M;
-  load_octant(oct, T.oct, T.logM);
+  double2* tw = smem + (size_t)a.rpc * M;
+  load_tw<LOGM>(tw, T.tw);
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
   const int row = blockIdx.x * a.rpc + grp;
   const bool valid = row < a.n_sets * per;
@@ -107,11 +111,11 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
   const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * a.n_bins;
   const double2* Gb = Ga + a.n_bins;
 
-  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+  for (int n0 = gtid; n0 < M; n0 += 8 * GS) {
     double2 x[8], c[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       x[u] = make_double2(0.0, 0.0);
       c[u] = make_double2(0.0, 0.0);
       if (valid && n < N) {
@@ -135,19 +139,19 @@ __global__ void phi_inv_kernel(PhiInvArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       if (n < M) buf[swz(n)] = cmulc(x[u], c[u]);
     }
   }
   __syncthreads();
-  fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
+  fft_conv<LOGM, GS>(buf, tw, T.bl_inv, gtid);
   if (!valid) return;
   const int pole_ring = (T.N + 1) / 2 - 1 - a.t_offset;  // local index of the MW pole ring
   const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
   const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
   const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
   const size_t ob = ((size_t)set * a.n_rings + ta) * N;
-  for (int q = gtid; q < N; q += a.gsize) {
+  for (int q = gtid; q < N; q += GS) {
     const double2 v = cmulc(buf[swz(q)], __ldg(&T.chirp[q]));
     if (a.real) {
       a.out[ob + q] = pa ? pva.x : v.x;
@@ -209,70 +213,72 @@ S2W_DEV void theta_store(const ThetaPair& P, const ThetaArgs& a, int t, double2 
   if (P.ho) P.ho[t] = cadd(cscale(csub(wt, wr), 0.5), dr);
 }
 
-__global__ void theta_kernel(ThetaArgs a) {
+template <int LOGM>
+__global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int M = 1 << T.logM, N = T.N, k = a.k;
-  const int grp = threadIdx.x / a.gsize, gtid = threadIdx.x - grp * a.gsize;
+  constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
+  const int N = T.N, k = a.k;
+  const int grp = threadIdx.x / GS, gtid = threadIdx.x % GS;
   double2* buf = smem + (size_t)grp * M;
-  double2* oct = smem + (size_t)a.rpc * M;
-  load_octant(oct, T.oct, T.logM);
+  double2* tw = smem + (size_t)a.rpc * M;
+  load_tw<LOGM>(tw, T.tw);
   const int row = blockIdx.x * a.rpc + grp;
   const bool valid = row < a.n_sets * a.n_pairs;
   const ThetaPair P = theta_pair(a, row, valid);
 
   // 1. parity extension to the full circle, times the Bluestein chirp
-  for (int n0 = gtid; n0 < M; n0 += 8 * a.gsize) {
+  for (int n0 = gtid; n0 < M; n0 += 8 * GS) {
     double2 x[8], c[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       const bool in = valid && n < N;
       x[u] = in ? theta_ext(P, n, k) : make_double2(0.0, 0.0);
       c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u * a.gsize;
+      const int n = n0 + u * GS;
       if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
     }
   }
   __syncthreads();
   // 2. DFT_N (Bluestein)
-  fft_conv(buf, T.logM, oct, T.bl_fwd, gtid, a.gsize);
+  fft_conv<LOGM, GS>(buf, tw, T.bl_fwd, gtid);
   // 3. Fourier coefficients a_{m'} = c_bin e^{-i pi m'/N} conv[bin] / N, laid out
   //    over the length-M circle (negative m' at the top)
-  for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
+  for (int b0 = gtid; b0 < N; b0 += 8 * GS) {
     double2 ph[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * a.gsize;
+      const int bin = b0 + u * GS;
       ph[u] = (bin < N) ? __ldg(&T.ph1[bin]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * a.gsize;
+      const int bin = b0 + u * GS;
       if (bin >= N) continue;
       const double2 v = cmul(buf[swz(bin)], ph[u]);
       buf[swz(bin < k ? bin : M - N + bin)] = v;
     }
   }
   __syncthreads();
-  for (int n = k + gtid; n < M - k + 1; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
+  for (int n = k + gtid; n < M - k + 1; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 4. convolution with the |sin theta| series (precomputed spectrum)
-  fft_conv(buf, T.logM, oct, T.wconv, gtid, a.gsize);
+  fft_conv<LOGM, GS>(buf, tw, T.wconv, gtid);
   // 5. back onto N bins with the e^{i pi q/N} offset phase and the inverse chirp
-  for (int b0 = gtid; b0 < N; b0 += 8 * a.gsize) {
+  for (int b0 = gtid; b0 < N; b0 += 8 * GS) {
     double2 ph[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * a.gsize;
+      const int bin = b0 + u * GS;
       ph[u] = (bin < N) ? __ldg(&T.ph2[bin]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * a.gsize;
+      const int bin = b0 + u * GS;
       if (bin >= N) continue;
       // bins >= k read from [M-k+1, M), disjoint from the written range [k, N)
       const double2 v = (bin < k) ? buf[swz(bin)] : buf[swz(M - N + bin)];
@@ -280,12 +286,12 @@ __global__ void theta_kernel(ThetaArgs a) {
     }
   }
   __syncthreads();
-  for (int n = N + gtid; n < M; n += a.gsize) buf[swz(n)] = make_double2(0.0, 0.0);
+  for (int n = N + gtid; n < M; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
-  fft_conv(buf, T.logM, oct, T.bl_inv, gtid, a.gsize);
+  fft_conv<LOGM, GS>(buf, tw, T.bl_inv, gtid);
   if (!valid) return;
-  for (int t = gtid; t < k; t += a.gsize) {
+  for (int t = gtid; t < k; t += GS) {
     const int tr = N - 1 - t;
     const double2 wt = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
     const double2 wr = cmulc(buf[swz(tr)], __ldg(&T.chirp[tr]));
@@ -304,14 +310,15 @@ __global__ void theta_kernel(ThetaArgs a) {
 // =====================================================================
 constexpr int SPLIT_T = 512;
 
-template <class Fill>
+template <int LOGF, class Fill>
 S2W_DEV void split_conv(double2* buf, double2* u_out, const double2* __restrict__ tab,
-                        int logF, const double2* octF, Fill fill) {
-  const int F = 1 << logF;
+                        const double2* twF, Fill fill) {
+  static_assert(fft_gs(LOGF) == SPLIT_T, "split mode runs one engine row per CTA");
+  constexpr int F = 1 << LOGF;
   for (int half = 0; half < 2; ++half) {
     fill(half);
     __syncthreads();
-    fft_conv(buf, logF, octF, tab + half * F, threadIdx.x, SPLIT_T);
+    fft_conv<LOGF, SPLIT_T>(buf, twF, tab + half * F, threadIdx.x);
     if (half == 0) {
       for (int j = threadIdx.x; j < F; j += SPLIT_T) u_out[j] = buf[swz(j)];
       __syncthreads();
@@ -321,14 +328,16 @@ S2W_DEV void split_conv(double2* buf, double2* u_out, const double2* __restrict_
 
 S2W_DEV double2 wM(int j, const double2* octM, int logM) { return twiddle(j, octM, logM); }
 
+template <int LOGF>
 __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
+  constexpr int logM = LOGF + 1, F = 1 << LOGF;
+  const int N = T.N;
   double2* buf = smem;
-  double2* octF = smem + F;
-  double2* octM = octF + oct_alloc(logF);
-  load_octant(octF, T.oct, logF);
+  double2* twF = smem + F;
+  double2* octM = twF + ((fft_ntw(LOGF) + 7) & ~7);
+  load_tw<LOGF>(twF, T.tw);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
@@ -339,7 +348,7 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
     const int ta = a.real ? 2 * p : p;
     const bool vb = a.real && ta + 1 < a.n_rings;
     const long long base_a = ((long long)set * a.n_rings + ta) * N;
-    split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
+    split_conv<LOGF>(buf, u, T.bl_fwd, twF, [&](int half) {
       for (int j = threadIdx.x; j < F; j += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (j < N) {
@@ -370,14 +379,16 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
   }
 }
 
+template <int LOGF>
 __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N;
+  constexpr int logM = LOGF + 1, F = 1 << LOGF;
+  const int N = T.N;
   double2* buf = smem;
-  double2* octF = smem + F;
-  double2* octM = octF + oct_alloc(logF);
-  load_octant(octF, T.oct, logF);
+  double2* twF = smem + F;
+  double2* octM = twF + ((fft_ntw(LOGF) + 7) & ~7);
+  load_tw<LOGF>(twF, T.tw);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
     const bool vb = a.real && ta + 1 < a.n_rings;
     const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * a.n_bins;
     const double2* Gb = Ga + a.n_bins;
-    split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
+    split_conv<LOGF>(buf, u, T.bl_inv, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (n < N) {
@@ -432,14 +443,16 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
   }
 }
 
+template <int LOGF>
 __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
-  const int logM = T.logM, logF = logM - 1, F = 1 << logF, N = T.N, k = a.k;
+  constexpr int logM = LOGF + 1, F = 1 << LOGF;
+  const int N = T.N, k = a.k;
   double2* buf = smem;
-  double2* octF = smem + F;
-  double2* octM = octF + oct_alloc(logF);
-  load_octant(octF, T.oct, logF);
+  double2* twF = smem + F;
+  double2* octM = twF + ((fft_ntw(LOGF) + 7) & ~7);
+  load_tw<LOGF>(twF, T.tw);
   load_octant(octM, T.octM, logM);
   double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;   // even-half results
   double2* sv = u + F;                                  // saved row (a_bin, then X_bin)
@@ -448,7 +461,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
     const ThetaPair P = theta_pair(a, row, true);
     // 1-2. DFT_N of the parity extension (Bluestein)
-    split_conv(buf, u, T.bl_fwd, logF, octF, [&](int half) {
+    split_conv<LOGF>(buf, u, T.bl_fwd, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         if (n < N) {
@@ -465,7 +478,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
     }
     __syncthreads();
     // 4. |sin| convolution of A (A_q = a_q for q < k, A_{M-N+b} = a_b for b >= k)
-    split_conv(buf, u, T.wconv, logF, octF, [&](int half) {
+    split_conv<LOGF>(buf, u, T.wconv, twF, [&](int half) {
       for (int j = threadIdx.x; j < F; j += SPLIT_T) {
         double2 v = make_double2(0.0, 0.0);
         double sign = 1.0;
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
     }
     __syncthreads();
     // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
-    split_conv(buf, u, T.bl_inv, logF, octF, [&](int half) {
+    split_conv<LOGF>(buf, u, T.bl_inv, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
         double2 v = (n < N) ? sv[n] : make_double2(0.0, 0.0);
         if (half && n < N) v = cmul(v, wM(n, octM, logM));
@@ -510,32 +523,59 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
 }
 
 // ---------------------------------------------------------------- launchers
-static void fft_geometry(int logM, int max_rows_smem, int& gsize, int& rpc, size_t& smem) {
-  const int M = 1 << logM;
-  gsize = M / 8;
-  if (gsize > 512) gsize = 512;
-  if (gsize < 1) gsize = 1;
-  rpc = 1;
-  while (rpc * gsize < 128 && (size_t)(rpc * 2) * M * sizeof(double2) <= 64 * 1024 &&
-         rpc * 2 <= max_rows_smem)
-    rpc *= 2;
-  smem = ((size_t)rpc * M + oct_alloc(logM)) * sizeof(double2);
-}
-
 static cudaError_t set_smem(const void* fn, size_t smem) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-static int split_grid(int n_rows) {
+static int device_sms() {
   int dev, sms;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return n_rows < sms ? n_rows : sms;
+  return sms;
+}
+
+// Rows per CTA for the shared-memory kernels: the value (<= fft_maxthr threads
+// per CTA) that maximises resident threads per SM, given the kernel's registers
+// and the shared memory per row.
+static int pick_rpc(const void* fn, int logm, int n_rows, size_t& smem) {
+  const int M = 1 << logm, gs = fft_gs(logm);
+  const size_t tw = (size_t)((fft_ntw(logm) + 7) & ~7) * sizeof(double2);
+  cudaFuncAttributes fa;
+  int regs = 128;
+  if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
+  int best = 1, best_occ = -1;
+  for (int rpc = 1; rpc * gs <= fft_maxthr(logm) && rpc <= n_rows; rpc *= 2) {
+    const int threads = rpc * gs;
+    const size_t sm = (size_t)rpc * M * sizeof(double2) + tw;
+    if (sm > 227 * 1024) break;
+    const int by_smem = (int)((228 * 1024) / (sm + 1024));
+    const int by_regs = 65536 / (threads * ((regs + 7) & ~7));
+    const int by_thr = 2048 / threads;
+    const int ctas = std::min(std::min(by_smem, by_regs), std::min(by_thr, 32));
+    const int occ = ctas * threads;
+    if (occ > best_occ) {
+      best_occ = occ;
+      best = rpc;
+    }
+  }
+  smem = (size_t)best * M * sizeof(double2) + tw;
+  return best;
+}
+
+template <class Args>
+static cudaError_t row_launch(void (*kern)(Args), int logm, Args a, int n_rows, cudaStream_t st) {
+  size_t smem;
+  a.rpc = pick_rpc((const void*)kern, logm, n_rows, smem);
+  cudaError_t e = set_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (n_rows + a.rpc - 1) / a.rpc;
+  kern<<<grid, a.rpc * fft_gs(logm), smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 static size_t split_smem(int logM) {
   const int F = 1 << (logM - 1);
-  return ((size_t)F + oct_alloc(logM - 1) + oct_alloc(logM)) * sizeof(double2);
+  return ((size_t)F + ((fft_ntw(logM - 1) + 7) & ~7) + oct_alloc(logM)) * sizeof(double2);
 }
 
 template <class Args>
@@ -544,42 +584,46 @@ static cudaError_t split_launch(void (*kern)(Args), Args a, int n_rows, cudaStre
   cudaError_t e = set_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   if (!a.scratch) return cudaErrorInvalidValue;
-  kern<<<split_grid(n_rows), SPLIT_T, smem, st>>>(a);
+  kern<<<std::min(n_rows, device_sms()), SPLIT_T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 size_t fft_split_scratch_elems(int logM) {
   if (logM <= FFT_MAX_LOGM_SMEM) return 0;
-  int dev, sms;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return (size_t)sms * 2 * ((size_t)1 << (logM - 1));
+  return (size_t)device_sms() * 2 * ((size_t)1 << (logM - 1));
 }
+
+int fft_tw_elems(int logE) { return fft_ntw(logE); }
+
+// Dispatch on the convolution size: shared-memory kernels for logM <= 13,
+// split mode for logM == 14.
+#define S2W_FFT_DISPATCH(KERN, SPLIT, ARGS, NROWS, ST)                      \
+  switch ((ARGS).T.logM) {                                                   \
+    case 3: return row_launch(KERN<3>, 3, ARGS, NROWS, ST);                  \
+    case 4: return row_launch(KERN<4>, 4, ARGS, NROWS, ST);                  \
+    case 5: return row_launch(KERN<5>, 5, ARGS, NROWS, ST);                  \
+    case 6: return row_launch(KERN<6>, 6, ARGS, NROWS, ST);                  \
+    case 7: return row_launch(KERN<7>, 7, ARGS, NROWS, ST);                  \
+    case 8: return row_launch(KERN<8>, 8, ARGS, NROWS, ST);                  \
+    case 9: return row_launch(KERN<9>, 9, ARGS, NROWS, ST);                  \
+    case 10: return row_launch(KERN<10>, 10, ARGS, NROWS, ST);               \
+    case 11: return row_launch(KERN<11>, 11, ARGS, NROWS, ST);               \
+    case 12: return row_launch(KERN<12>, 12, ARGS, NROWS, ST);               \
+    case 13: return row_launch(KERN<13>, 13, ARGS, NROWS, ST);               \
+    case 14: return split_launch(SPLIT<13>, ARGS, NROWS, ST);                \
+    default: return cudaErrorInvalidValue;                                   \
+  }
 
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
-  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_fwd_split_kernel, a, n_rows, st);
-  size_t smem;
-  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
-  cudaError_t e = set_smem((const void*)phi_fwd_kernel, smem);
-  if (e != cudaSuccess) return e;
-  const int grid = (n_rows + a.rpc - 1) / a.rpc;
-  phi_fwd_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
-  return cudaGetLastError();
+  S2W_FFT_DISPATCH(phi_fwd_kernel, phi_fwd_split_kernel, a, n_rows, st)
 }
 
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
-  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(phi_inv_split_kernel, a, n_rows, st);
-  size_t smem;
-  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
-  cudaError_t e = set_smem((const void*)phi_inv_kernel, smem);
-  if (e != cudaSuccess) return e;
-  const int grid = (n_rows + a.rpc - 1) / a.rpc;
-  phi_inv_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
-  return cudaGetLastError();
+  S2W_FFT_DISPATCH(phi_inv_kernel, phi_inv_split_kernel, a, n_rows, st)
 }
 
 void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
@@ -599,14 +643,7 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
-  if (a.T.logM > FFT_MAX_LOGM_SMEM) return split_launch(theta_split_kernel, a, n_rows, st);
-  size_t smem;
-  fft_geometry(a.T.logM, n_rows, a.gsize, a.rpc, smem);
-  cudaError_t e = set_smem((const void*)theta_kernel, smem);
-  if (e != cudaSuccess) return e;
-  const int grid = (n_rows + a.rpc - 1) / a.rpc;
-  theta_kernel<<<grid, a.rpc * a.gsize, smem, st>>>(a);
-  return cudaGetLastError();
+  S2W_FFT_DISPATCH(theta_kernel, theta_split_kernel, a, n_rows, st)
 }
 
 }  // namespace s2w

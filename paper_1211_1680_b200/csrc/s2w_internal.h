@@ -13,7 +13,7 @@ constexpr int FFT_MAX_LOGM_SMEM = 13;  // one 128 KiB row per CTA; larger M uses
 
 struct FftTablesDev {
   int N, logM;  // logM of the convolution length M; split mode when logM > 13
-  const double2* oct;     // octant twiddle table of the FFT engine size (M, or M/2 in split mode)
+  const double2* tw;      // radix-16 pass twiddles of the FFT engine size (M, or M/2 in split mode)
   const double2* octM;    // split mode: octant table of M (for W_M^j)
   const double2* chirp;   // [N]  c_n = exp(-i pi n^2/N)
   const double2* bl_fwd;  // [M]  FFT(conj c, circular)/M
@@ -63,6 +63,8 @@ struct ThetaArgs {
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
 // Scratch (double2 elements) the split-mode kernels need for convolution size 2^logM.
 size_t fft_split_scratch_elems(int logM);
+// Length of the pass-twiddle table of the FFT engine of size 2^logE.
+int fft_tw_elems(int logE);
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st);
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st);
 // Pair storage rows by the parity of their order m (bins[row] = azimuthal bin).

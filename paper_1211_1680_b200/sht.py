@@ -10,7 +10,7 @@ Public names, layouts and error behaviour follow the reference
   stage (the reference raises on MW, sht.py:300-303; here MW analysis is
   exact) and the deterministic ring reduction;
 * ``assoc_legendre_ring``   -> ``s2w_assoc_legendre_ring`` (extended-exponent
-  recursion, valid to L = 16383, unlike the reference's 1e-280 flush).
+  recursion, valid to L = 4096 (the FFT engine limit), unlike the reference's 1e-280 flush).
 
 Coefficients use the flat ``l*l + l + m`` layout; real-signal sets carry the
 exact conjugate symmetry ``f(l,-m) = (-1)^m conj f(l,m)``.
