@@ -322,13 +322,22 @@ static int device_tables(int dev, DeviceTables** out) {
 }
 
 // ------------------------------------------------------------------ grid resources
-struct GridRes {
-  int device, scheme, k, N, logM;
-  std::vector<int2> act_host;
+// A set of rings for the Legendre stages: nodes, analysis weights, active
+// ring range per order.  n_north > 0 marks an equator-symmetric set.
+struct RingSet {
   double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
   int2* act = nullptr;
+  std::vector<int2> act_host;
+  int n_north = 0;
+};
+
+struct GridRes {
+  int device, scheme, k, N, logM;
+  // syn: the sampling rings (synthesis output, GL analysis);
+  // ana: the analysis rings (GL: the GL rings; MW: theta''_j = (2j+1) pi / 2k, see theta_kernel)
+  RingSet syn, ana;
   double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
-          *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr;
+          *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
   int2 *pairs_r = nullptr, *pairs_c = nullptr;
@@ -358,26 +367,33 @@ struct GridRes {
     t.ph1 = ph1;
     t.ph2 = ph2;
     t.wconv = wconv;
+    t.N2 = 2 * k;
+    t.chirp2 = chirp2;
+    t.bl_ev = bl_ev;
     return t;
   }
-  LegGridDev leg(bool cplx) const {
+  LegGridDev leg(bool cplx, bool analysis) const {
+    const RingSet& rs = analysis ? ana : syn;
     LegGridDev g;
     g.k = k;
     g.n_t = k;
+    g.n_north = rs.n_north;
     g.n_bins = cplx ? N : k;
-    g.cos_t = cos_t;
-    g.sin_t = sin_t;
-    g.ring_w = ring_w;
-    g.act = act;
+    g.cos_t = rs.cos_t;
+    g.sin_t = rs.sin_t;
+    g.ring_w = rs.ring_w;
+    g.act = rs.act;
     g.binmap = nullptr;
     g.n_cols = cplx ? N : k;
     return g;
   }
   int n_bins(bool cplx) const { return cplx ? N : k; }
   // rough cost of the Legendre work for order m (ring-steps)
-  double cost(int m) const {
-    const int2 a = act_host[m];
-    return (double)(k - m) * (double)std::max(0, a.y - a.x) + 64.0;
+  double cost(int m, bool analysis) const {
+    const RingSet& rs = analysis ? ana : syn;
+    const int2 a = rs.act_host[m];
+    const int n = rs.n_north ? std::max(0, std::min(a.y, rs.n_north) - a.x) : std::max(0, a.y - a.x);
+    return (double)(k - m) * (double)n + 64.0;
   }
 };
 
@@ -387,6 +403,50 @@ template <class T>
 static int upload_new(T** dst, const std::vector<T>& v) {
   CU(cudaMalloc(dst, std::max<size_t>(16, v.size() * sizeof(T))));
   if (!v.empty()) CU(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return S2W_OK;
+}
+
+// Upload a ring set and find its active ring range per order (probe kernel).
+// Symmetric sets (n_north > 0) get exactly mirrored nodes: cos(pi - x) = -cos x.
+static int ring_set(RingSet& rs, const std::vector<double>& theta, const std::vector<double>& w,
+                    int k, const double* seed_c, int n_north) {
+  const int n = (int)theta.size();
+  std::vector<double> c(n), s(n);
+  for (int t = 0; t < n; ++t) {
+    c[t] = std::cos(theta[t]);
+    s[t] = std::sin(theta[t]);
+  }
+  if (n_north)
+    for (int t = n - n_north; t < n; ++t) {
+      const int tm = n - 1 - t;
+      if (tm == t) {
+        c[t] = 0.0;
+        continue;
+      }
+      c[t] = -c[tm];
+      s[t] = s[tm];
+    }
+  rs.n_north = n_north;
+  CHECK(upload_new(&rs.cos_t, c));
+  CHECK(upload_new(&rs.sin_t, s));
+  CHECK(upload_new(&rs.ring_w, w));
+  int* d_mmax = nullptr;
+  CU(cudaMalloc(&d_mmax, sizeof(int) * n));
+  CU(launch_leg_probe(k, n, rs.cos_t, rs.sin_t, seed_c, d_mmax, 0));
+  std::vector<int> mmax(n);
+  CU(cudaMemcpy(mmax.data(), d_mmax, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  cudaFree(d_mmax);
+  rs.act_host.assign(k, make_int2(0, 0));
+  for (int m = 0; m < k; ++m) {
+    int lo = -1, hi = -1;
+    for (int t = 0; t < n; ++t)
+      if (mmax[t] >= m) {
+        if (lo < 0) lo = t;
+        hi = t;
+      }
+    rs.act_host[m] = (lo < 0) ? make_int2(0, 0) : make_int2(lo, hi + 1);
+  }
+  CHECK(upload_new(&rs.act, rs.act_host));
   return S2W_OK;
 }
 
@@ -450,38 +510,25 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   std::vector<double> theta, wq;
   if (scheme == S2W_SCHEME_GL) gl_nodes(k, theta, wq);
   else mw_nodes(k, theta);
-  std::vector<double> c(k), s(k), rw(k);
+  std::vector<double> rw(k);
   for (int t = 0; t < k; ++t) {
-    c[t] = std::cos(theta[t]);
-    s[t] = std::sin(theta[t]);
     if (scheme == S2W_SCHEME_GL) rw[t] = 2.0 * M_PI * wq[t];
     else rw[t] = (2.0 * M_PI / (double)N) * (t == k - 1 ? 0.5 : 1.0);
   }
-  CHECK(upload_new(&g->cos_t, c));
-  CHECK(upload_new(&g->sin_t, s));
-  CHECK(upload_new(&g->ring_w, rw));
-
-  // active ring range per order (probe kernel, once per grid)
-  int* d_mmax = nullptr;
-  CU(cudaMalloc(&d_mmax, sizeof(int) * k));
-  CU(launch_leg_probe(k, k, g->cos_t, g->sin_t, g->seed_c, d_mmax, 0));
-  std::vector<int> mmax(k);
-  CU(cudaMemcpy(mmax.data(), d_mmax, sizeof(int) * k, cudaMemcpyDeviceToHost));
-  cudaFree(d_mmax);
-  g->act_host.assign(k, make_int2(0, 0));
-  for (int m = 0; m < k; ++m) {
-    int lo = -1, hi = -1;
-    for (int t = 0; t < k; ++t)
-      if (mmax[t] >= m) {
-        if (lo < 0) lo = t;
-        hi = t;
-      }
-    g->act_host[m] = (lo < 0) ? make_int2(0, 0) : make_int2(lo, hi + 1);
+  CHECK(ring_set(g->syn, theta, rw, k, g->seed_c, 0));
+  if (scheme == S2W_SCHEME_GL) {
+    g->ana = g->syn;  // same device tables; analysis uses the equator symmetry
+    g->ana.n_north = (k + 1) / 2;
+  } else {
+    // analysis rings of the MW theta stage: theta''_j = (2j+1) pi / 2k, weight pi / k
+    std::vector<double> th2(k), w2(k, M_PI / (double)k);
+    for (int j = 0; j < k; ++j) th2[j] = (double)((ld)(2 * j + 1) * PI_L / (ld)(2 * k));
+    CHECK(ring_set(g->ana, th2, w2, k, g->seed_c, (k + 1) / 2));
   }
-  CHECK(upload_new(&g->act, g->act_host));
 
   // FFT / Bluestein / theta-stage tables
-  std::vector<double2> chirp(N), ph1(N), ph2(N);
+  const int N2 = 2 * k;
+  std::vector<double2> chirp(N), ph1(N), ph2(N2), chirp2(N2);
   const bool split = g->logM > FFT_MAX_LOGM_SMEM;
   std::vector<cld> cl(N);
   for (int n = 0; n < N; ++n) {
@@ -507,7 +554,25 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     const int q = bin < k ? bin : bin - N;
     ld a1 = -PI_L * (ld)q / (ld)N;
     ph1[bin] = d2(cl[bin] * cld(std::cos(a1), std::sin(a1)) / (ld)N);
-    ph2[bin] = d2(cld(std::cos(-a1), std::sin(-a1)) * std::conj(cl[bin]));
+  }
+  // evaluation on the analysis rings: inverse DFT of length N2 = 2k (Bluestein)
+  std::vector<cld> c2(N2), cc2(M, cld(0, 0));
+  for (int n = 0; n < N2; ++n) {
+    const long long r = ((long long)n * n) % (2LL * N2);
+    const ld ang = -PI_L * (ld)r / (ld)N2;
+    c2[n] = cld(std::cos(ang), std::sin(ang));
+    chirp2[n] = d2(c2[n]);
+    cc2[n] = c2[n];
+    if (n > 0) cc2[M - n] = c2[n];
+  }
+  for (int n = 0; n < N2; ++n) {
+    const int q = n < k ? n : n - N2;
+    if (n >= k && n <= N2 - k) {
+      ph2[n] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const ld a2 = PI_L * (ld)q / (ld)N2;
+    ph2[n] = d2(cld(std::cos(a2), std::sin(a2)) * std::conj(c2[n]));
   }
   CHECK(upload_new(&g->tw, pass_twiddles(split ? g->logM - 1 : g->logM)));
   if (split) CHECK(upload_new(&g->octM, octant_table(g->logM)));
@@ -517,6 +582,8 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->wconv, spectrum_brev(w)));
   CHECK(upload_new(&g->ph1, ph1));
   CHECK(upload_new(&g->ph2, ph2));
+  CHECK(upload_new(&g->chirp2, chirp2));
+  CHECK(upload_new(&g->bl_ev, spectrum_brev(cc2)));
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   g_grids[key] = g;
   *out = g;
@@ -564,7 +631,7 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   const int ns = pick_ns(maxn, cplx);
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const auto& gr = groups[gi];
-    grids.push_back(gr.g->leg(cplx));
+    grids.push_back(gr.g->leg(cplx, false));
     const int base = (int)sets.size();
     for (auto& s : gr.sets) sets.push_back(s);
     const int n = (int)gr.sets.size();
@@ -572,7 +639,7 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
       for (int s0 = 0; s0 < n; s0 += ns) {
         const int nset = std::min(ns, n - s0);
         SynthItem it{(int)gi, m, base + s0, nset};
-        items.push_back({it, gr.g->cost(m) * (3.0 + 4.0 * ns)});
+        items.push_back({it, gr.g->cost(m, false) * (3.0 + 4.0 * ns)});
       }
   }
   std::stable_sort(items.begin(), items.end(),
@@ -606,7 +673,7 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   for (auto& s : segspecs)
     if (std::find(gl.begin(), gl.end(), s.g) == gl.end()) gl.push_back(s.g);
   std::vector<LegGridDev> grids;
-  for (auto* g : gl) grids.push_back(g->leg(cplx));
+  for (auto* g : gl) grids.push_back(g->leg(cplx, true));
   int maxn = 1, kmax = 0;
   for (auto& s : segspecs) maxn = std::max<int>(maxn, (int)s.sets.size());
   for (auto* g : gl) kmax = std::max(kmax, g->k);
@@ -643,7 +710,7 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
       if (m >= g->k) continue;
       segs.push_back(sg);
       ++it.nseg;
-      cost += g->cost(m) * (3.0 + 4.0 * ns);
+      cost += g->cost(m, true) * (3.0 + 4.0 * ns);
     }
     if (it.nseg) items.push_back({it, cost});
   }

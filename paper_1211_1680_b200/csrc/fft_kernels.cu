@@ -10,7 +10,9 @@
 //  theta_kernel   : MW forward theta stage per order m (absent from the reference,
 //                   whose MW analysis raises at sht.py:300-303): parity extension to
 //                   the full circle, DFT_N, convolution with the Fourier series of
-//                   |sin theta|, inverse DFT_N on the first L rings.  See DESIGN.md.
+//                   |sin theta|, and evaluation of the result on the L analysis rings
+//                   theta''_j = (2j+1) pi / 2L (an inverse DFT of length 2L), which are
+//                   symmetric about the equator.  See DESIGN.md.
 //
 // All odd-length DFTs (N = 2L-1) are Bluestein chirp-z transforms over the
 // power-of-two shared-memory FFT in fft.cuh.
@@ -268,33 +270,38 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
   __syncthreads();
   // 4. convolution with the |sin theta| series (precomputed spectrum)
   fft_conv<LOGM, GS>(buf, tw, T.wconv, gtid);
-  // 5. back onto N bins with the e^{i pi q/N} offset phase and the inverse chirp
-  for (int b0 = gtid; b0 < N; b0 += 8 * GS) {
+  // 5. evaluation on the analysis rings theta''_j = (2j+1) pi / N2 (N2 = 2k):
+  //    Bluestein input X_n = H'(q) e^{i pi q/N2} conj(c2_n), n = q mod N2.
+  //    H'(q) sits at q (q >= 0) and M + q (q < 0); the moves read [M-k+1, M)
+  //    and write [k, N2), disjoint.
+  const int N2 = T.N2;
+  for (int n0 = gtid; n0 < N2; n0 += 8 * GS) {
     double2 ph[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * GS;
-      ph[u] = (bin < N) ? __ldg(&T.ph2[bin]) : make_double2(0.0, 0.0);
+      const int n = n0 + u * GS;
+      ph[u] = (n < N2) ? __ldg(&T.ph2[n]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int bin = b0 + u * GS;
-      if (bin >= N) continue;
-      // bins >= k read from [M-k+1, M), disjoint from the written range [k, N)
-      const double2 v = (bin < k) ? buf[swz(bin)] : buf[swz(M - N + bin)];
-      buf[swz(bin)] = cmul(v, ph[u]);
+      const int n = n0 + u * GS;
+      if (n >= N2) continue;
+      const double2 v = (n < k) ? buf[swz(n)]
+                                : (n > N2 - k ? buf[swz(M - N2 + n)] : make_double2(0.0, 0.0));
+      buf[swz(n)] = cmul(v, ph[u]);
     }
   }
   __syncthreads();
-  for (int n = N + gtid; n < M; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
+  for (int n = N2 + gtid; n < M; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
-  // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
-  fft_conv<LOGM, GS>(buf, tw, T.bl_inv, gtid);
+  // 6. inverse DFT_N2 (Bluestein); rings j and N2-1-j (its mirror 2 pi - theta''_j),
+  //    split by parity
+  fft_conv<LOGM, GS>(buf, tw, T.bl_ev, gtid);
   if (!valid) return;
   for (int t = gtid; t < k; t += GS) {
-    const int tr = N - 1 - t;
-    const double2 wt = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
-    const double2 wr = cmulc(buf[swz(tr)], __ldg(&T.chirp[tr]));
+    const int tr = N2 - 1 - t;
+    const double2 wt = cmulc(buf[swz(t)], __ldg(&T.chirp2[t]));
+    const double2 wr = cmulc(buf[swz(tr)], __ldg(&T.chirp2[tr]));
     theta_store(P, a, t, wt, wr);
   }
 }
@@ -492,31 +499,33 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
         buf[swz(j)] = v;
       }
     });
-    // 5. X_bin = H'(q) e^{i pi q/N} conj(c_bin); q = bin (bin < k) or bin - N
-    for (int b = threadIdx.x; b < N; b += SPLIT_T) {
-      double2 h;
-      if (b < k) {
-        h = cadd(u[b], cmulc(buf[swz(b)], wM(b, octM, logM)));
-      } else {
-        const int j = F + b - N;  // position M + q = j + F
+    // 5. evaluation input on the analysis rings (see theta_kernel):
+    //    X_n = H'(q) e^{i pi q/N2} conj(c2_n), q = n (n < k) or n - N2 (n > N2 - k)
+    const int N2 = T.N2;
+    for (int n = threadIdx.x; n < N2; n += SPLIT_T) {
+      double2 h = make_double2(0.0, 0.0);
+      if (n < k) {
+        h = cadd(u[n], cmulc(buf[swz(n)], wM(n, octM, logM)));
+      } else if (n > N2 - k) {
+        const int j = F + n - N2;  // position M + q = j + F
         h = csub(u[j], cmulc(buf[swz(j)], wM(j, octM, logM)));
       }
-      sv[b] = cmul(h, __ldg(&T.ph2[b]));
+      sv[n] = cmul(h, __ldg(&T.ph2[n]));
     }
     __syncthreads();
-    // 6. inverse DFT_N (Bluestein); rings t and N-1-t, split by parity
-    split_conv<LOGF>(buf, u, T.bl_inv, twF, [&](int half) {
+    // 6. inverse DFT_N2 (Bluestein); rings t and N2-1-t, split by parity
+    split_conv<LOGF>(buf, u, T.bl_ev, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
-        double2 v = (n < N) ? sv[n] : make_double2(0.0, 0.0);
-        if (half && n < N) v = cmul(v, wM(n, octM, logM));
+        double2 v = (n < N2) ? sv[n] : make_double2(0.0, 0.0);
+        if (half && n < N2) v = cmul(v, wM(n, octM, logM));
         buf[swz(n)] = v;
       }
     });
     for (int t = threadIdx.x; t < k; t += SPLIT_T) {
-      const int tr = N - 1 - t;
+      const int tr = N2 - 1 - t;
       const double2 zt = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
       const double2 zr = cadd(u[tr], cmulc(buf[swz(tr)], wM(tr, octM, logM)));
-      theta_store(P, a, t, cmulc(zt, __ldg(&T.chirp[t])), cmulc(zr, __ldg(&T.chirp[tr])));
+      theta_store(P, a, t, cmulc(zt, __ldg(&T.chirp2[t])), cmulc(zr, __ldg(&T.chirp2[tr])));
     }
     __syncthreads();
   }

@@ -19,8 +19,12 @@ struct FftTablesDev {
   const double2* bl_fwd;  // [M]  FFT(conj c, circular)/M
   const double2* bl_inv;  // [M]  FFT(c, circular)/M
   const double2* ph1;     // [N]  c_b exp(-i pi m'(b)/N)/N      (MW theta stage)
-  const double2* ph2;     // [N]  exp(i pi q(b)/N) conj(c_b)    (MW theta stage)
   const double2* wconv;   // [M]  FFT(w_hat, circular)/M, w_hat(p)=4/(1-p^2) p even
+  // MW theta stage output on the analysis rings theta''_j = (2j+1) pi / N2, N2 = 2k:
+  int N2;
+  const double2* chirp2;  // [N2] c2_n = exp(-i pi n^2/N2)
+  const double2* bl_ev;   // [M]  FFT(c2, circular)/M
+  const double2* ph2;     // [N2] exp(i pi q(n)/N2) conj(c2_n), q(n) = n or n - N2 (|q| < k)
 };
 
 struct PhiFwdArgs {
@@ -74,6 +78,7 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs);
 struct LegGridDev {
   int k;       // band limit of the grid = number of orders / degrees
   int n_t;     // number of rings
+  int n_north; // > 0: rings symmetric about the equator (t <-> n_t-1-t), n_north = ceil(n_t/2)
   int n_bins;  // azimuthal bins stored per ring: 2k-1 (complex) or k (real)
   const double* cos_t;
   const double* sin_t;
