@@ -609,7 +609,7 @@ struct AnaCfg {
   bool built = false;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, segs, items;
-  int n_items = 0, ns = 1, cplx = 1, win = 32;
+  int n_items = 0, ns = 1, cplx = 1, win = 32, sym = 0;
 };
 
 // A synthesis "group": sets sharing one grid.
@@ -674,6 +674,8 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
     if (std::find(gl.begin(), gl.end(), s.g) == gl.end()) gl.push_back(s.g);
   std::vector<LegGridDev> grids;
   for (auto* g : gl) grids.push_back(g->leg(cplx, true));
+  cfg.sym = 1;
+  for (auto& gd : grids) cfg.sym &= gd.n_north > 0 ? 1 : 0;
   int maxn = 1, kmax = 0;
   for (auto& s : segspecs) maxn = std::max<int>(maxn, (int)s.sets.size());
   for (auto* g : gl) kmax = std::max(kmax, g->k);
@@ -759,6 +761,7 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
   a.win = cfg.win;
+  a.sym = cfg.sym;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_ANA, st);
   CU(launch_leg_ana(a, st));

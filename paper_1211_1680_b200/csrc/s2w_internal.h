@@ -145,6 +145,7 @@ struct LegAnaArgs {
   int cplx;
   int ns;
   int win;  // degrees per window (leg_ana_window)
+  int sym;  // every grid is equator-symmetric (LegGridDev::n_north > 0)
   double2* bufs[S2W_NBUF];
 };
 
