@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -679,7 +680,9 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   int maxn = 1, kmax = 0;
   for (auto& s : segspecs) maxn = std::max<int>(maxn, (int)s.sets.size());
   for (auto* g : gl) kmax = std::max(kmax, g->k);
-  const int ns = pick_ns(maxn, cplx);
+  // symmetric rings: at most 16 reals per degree (the symmetric DMMA kernel's
+  // two operand sets must fit the registers); wider batches become segments
+  const int ns = cfg.sym ? std::min(pick_ns(maxn, cplx), cplx ? 4 : 8) : pick_ns(maxn, cplx);
   // split segments wider than ns
   std::vector<AnaSet> sets;
   std::vector<AnaSeg> segs0;
@@ -704,17 +707,36 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   };
   std::vector<AnaSeg> segs;
   std::vector<It> items;
-  for (int m = 0; m < kmax; ++m) {
-    AnaItem it{m, (int)segs.size(), 0};
-    double cost = 0;
-    for (auto& sg : segs0) {
-      const GridRes* g = gl[sg.grid];
-      if (m >= g->k) continue;
-      segs.push_back(sg);
-      ++it.nseg;
-      cost += g->cost(m, true) * (3.0 + 4.0 * ns);
+  // Segments that accumulate into a common output share an item (their folds
+  // run in order inside one CTA); segments with disjoint outputs get an item
+  // (CTA) each.  Components by union-find over shared outputs.
+  const int nsg = (int)segs0.size();
+  std::vector<int> comp(nsg);
+  for (int i = 0; i < nsg; ++i) comp[i] = i;
+  std::function<int(int)> root = [&](int i) { return comp[i] == i ? i : comp[i] = root(comp[i]); };
+  std::map<std::pair<int, long long>, int> owner;
+  for (int i = 0; i < nsg; ++i)
+    for (int q = 0; q < segs0[i].nset; ++q) {
+      const AnaSet& S = sets[segs0[i].set0 + q];
+      auto key = std::make_pair(S.ob, S.ooff);
+      auto f = owner.find(key);
+      if (f == owner.end()) owner[key] = i;
+      else comp[root(i)] = root(f->second);
     }
-    if (it.nseg) items.push_back({it, cost});
+  for (int m = 0; m < kmax; ++m) {
+    for (int c0 = 0; c0 < nsg; ++c0) {
+      if (root(c0) != c0) continue;
+      AnaItem it{m, (int)segs.size(), 0};
+      double cost = 0;
+      for (int i = 0; i < nsg; ++i) {
+        const GridRes* g = gl[segs0[i].grid];
+        if (root(i) != c0 || m >= g->k) continue;
+        segs.push_back(segs0[i]);
+        ++it.nseg;
+        cost += g->cost(m, true) * (3.0 + 4.0 * ns);
+      }
+      if (it.nseg) items.push_back({it, cost});
+    }
   }
   std::stable_sort(items.begin(), items.end(),
                    [](const It& a, const It& b) { return a.cost > b.cost; });
