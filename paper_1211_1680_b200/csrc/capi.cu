@@ -338,7 +338,8 @@ struct GridRes {
   // ana: the analysis rings (GL: the GL rings; MW: theta''_j = (2j+1) pi / 2k, see theta_kernel)
   RingSet syn, ana;
   double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
-          *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr;
+          *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr,
+          *bl_fwd2 = nullptr, *ph4 = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
   int2 *pairs_r = nullptr, *pairs_c = nullptr;
@@ -371,10 +372,15 @@ struct GridRes {
     t.N2 = 2 * k;
     t.chirp2 = chirp2;
     t.bl_ev = bl_ev;
+    t.bl_fwd2 = bl_fwd2;
+    t.ph4 = ph4;
     return t;
   }
+  // MW synthesis runs on the (symmetric) analysis rings and is resampled to
+  // the MW rings by theta_syn_kernel; GL synthesis runs on its own rings.
+  bool syn_on_ana() const { return scheme == S2W_SCHEME_MW; }
   LegGridDev leg(bool cplx, bool analysis) const {
-    const RingSet& rs = analysis ? ana : syn;
+    const RingSet& rs = (analysis || syn_on_ana()) ? ana : syn;
     LegGridDev g;
     g.k = k;
     g.n_t = k;
@@ -386,12 +392,13 @@ struct GridRes {
     g.act = rs.act;
     g.binmap = nullptr;
     g.n_cols = cplx ? N : k;
+    g.mmajor = (!analysis && syn_on_ana()) ? 1 : 0;
     return g;
   }
   int n_bins(bool cplx) const { return cplx ? N : k; }
   // rough cost of the Legendre work for order m (ring-steps)
   double cost(int m, bool analysis) const {
-    const RingSet& rs = analysis ? ana : syn;
+    const RingSet& rs = (analysis || syn_on_ana()) ? ana : syn;
     const int2 a = rs.act_host[m];
     const int n = rs.n_north ? std::max(0, std::min(a.y, rs.n_north) - a.x) : std::max(0, a.y - a.x);
     return (double)(k - m) * (double)n + 64.0;
@@ -518,8 +525,8 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   }
   CHECK(ring_set(g->syn, theta, rw, k, g->seed_c, 0));
   if (scheme == S2W_SCHEME_GL) {
-    g->ana = g->syn;  // same device tables; analysis uses the equator symmetry
-    g->ana.n_north = (k + 1) / 2;
+    g->syn.n_north = (k + 1) / 2;  // GL nodes are symmetric about the equator
+    g->ana = g->syn;                // same device tables
   } else {
     // analysis rings of the MW theta stage: theta''_j = (2j+1) pi / 2k, weight pi / k
     std::vector<double> th2(k), w2(k, M_PI / (double)k);
@@ -566,6 +573,20 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     cc2[n] = c2[n];
     if (n > 0) cc2[M - n] = c2[n];
   }
+  std::vector<cld> b2(M, cld(0, 0));
+  for (int n = 0; n < N2; ++n) {
+    b2[n] = std::conj(c2[n]);
+    if (n > 0) b2[M - n] = std::conj(c2[n]);
+  }
+  // synthesis resampling: X_n = DFT_N2[src] ph4[n], n < N (see theta_syn_kernel)
+  std::vector<double2> ph4(N);
+  for (int n = 0; n < N; ++n) {
+    const int q = n < k ? n : n - N;
+    const int src = q >= 0 ? q : N2 + q;
+    const ld a2 = -PI_L * (ld)q / (ld)N2, a1 = PI_L * (ld)q / (ld)N;
+    ph4[n] = d2(c2[src] * cld(std::cos(a2), std::sin(a2)) * cld(std::cos(a1), std::sin(a1)) *
+                std::conj(cl[n]) / (ld)N2);
+  }
   for (int n = 0; n < N2; ++n) {
     const int q = n < k ? n : n - N2;
     if (n >= k && n <= N2 - k) {
@@ -585,6 +606,8 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->ph2, ph2));
   CHECK(upload_new(&g->chirp2, chirp2));
   CHECK(upload_new(&g->bl_ev, spectrum_brev(cc2)));
+  CHECK(upload_new(&g->bl_fwd2, spectrum_brev(b2)));
+  CHECK(upload_new(&g->ph4, ph4));
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   g_grids[key] = g;
   *out = g;
@@ -603,7 +626,7 @@ struct SynthCfg {
   bool built = false;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, items;
-  int n_items = 0, ns = 1, cplx = 1, win = 32;
+  int n_items = 0, ns = 1, cplx = 1, win = 32, sym = 0;
 };
 
 struct AnaCfg {
@@ -629,7 +652,10 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   std::vector<It> items;
   int maxn = 1;
   for (auto& gr : groups) maxn = std::max<int>(maxn, (int)gr.sets.size());
-  const int ns = pick_ns(maxn, cplx);
+  cfg.sym = 1;
+  for (auto& gr : groups) cfg.sym &= gr.g->leg(cplx, false).n_north > 0 ? 1 : 0;
+  // symmetric rings keep two accumulator sets: at most 4 complex / 8 real sets per CTA
+  const int ns = cfg.sym ? std::min(pick_ns(maxn, cplx), cplx ? 4 : 8) : pick_ns(maxn, cplx);
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const auto& gr = groups[gi];
     grids.push_back(gr.g->leg(cplx, false));
@@ -765,6 +791,7 @@ static int run_synth(const SynthCfg& cfg, const double* seed_c, double2* const* 
   a.cplx = cfg.cplx;
   a.ns = cfg.ns;
   a.win = cfg.win;
+  a.sym = cfg.sym;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_SYNTH, st);
   CU(launch_leg_synth(a, st));
@@ -821,8 +848,28 @@ static int forward_rings(const GridRes* g, int n_sets, bool real, const double* 
 }
 
 // G ring-major [n_sets][k][n_bins] -> map [n_sets][k][N]
-static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
-                         double2* scratch, cudaStream_t st) {
+// Resample synthesis output from the analysis rings (m-major) to the MW rings
+// (ring-major): theta_syn_kernel.
+static int theta_resample(const GridRes* g, int n_sets, bool real, const double2* Gm,
+                          double2* Gr, double2* scratch, cudaStream_t st) {
+  ThetaSynArgs ta;
+  ta.T = g->fft();
+  ta.n_sets = n_sets;
+  ta.k = g->k;
+  ta.n_bins = g->n_bins(!real);
+  ta.pairs = real ? g->pairs_r : g->pairs_c;
+  ta.n_pairs = real ? g->np_r : g->np_c;
+  ta.in = Gm;
+  ta.out = Gr;
+  ta.scratch = scratch;
+  ProfScope ps(P_THETA, st);
+  CU(launch_theta_syn(ta, st));
+  return S2W_OK;
+}
+
+// Ring-major G on the sampling rings -> maps (ring DFTs, MW pole pin).
+static int phi_inverse(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
+                       double2* scratch, cudaStream_t st) {
   PhiInvArgs pa;
   pa.scratch = scratch;
   pa.T = g->fft();
@@ -839,11 +886,22 @@ static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2*
   return S2W_OK;
 }
 
+// Legendre synthesis output G -> maps.  MW: G is m-major on the analysis
+// rings and is first resampled into tmp (ring-major, MW rings).
+static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
+                         double2* scratch, double2* tmp, cudaStream_t st) {
+  if (g->syn_on_ana()) {
+    CHECK(theta_resample(g, n_sets, real, G, tmp, scratch, st));
+    G = tmp;
+  }
+  return phi_inverse(g, n_sets, real, G, map, scratch, st);
+}
+
 // ------------------------------------------------------------------ SHT plan
 struct s2w_sht_plan {
   int device, scheme, L;
   GridRes* g;
-  DevBuf G, scratch;
+  DevBuf G, G2, scratch;  // G2: MW resampling target
   SynthCfg syn;
   AnaCfg ana;
 };
@@ -946,7 +1004,9 @@ int s2w_sh_synthesis(s2w_sht_plan* p, int n_sets, int L_coef, int is_real, const
   }
   double2* bufs[S2W_NBUF] = {(double2*)flm, p->G.as<double2>(), nullptr, nullptr};
   CHECK(run_synth(c, g->seed_c, bufs, st));
-  CHECK(inverse_rings(g, n_sets, !cplx, p->G.as<double2>(), map, p->scratch.as<double2>(), st));
+  if (g->syn_on_ana()) CHECK(p->G2.ensure(sizeof(double2) * (size_t)n_sets * nb * k));
+  CHECK(inverse_rings(g, n_sets, !cplx, p->G.as<double2>(), map, p->scratch.as<double2>(),
+                      p->G2.as<double2>(), st));
   return S2W_OK;
 }
 
@@ -997,7 +1057,7 @@ struct s2w_wav_plan {
   GridRes* top = nullptr;             // grid at L
   std::vector<GridRes*> kgrid;        // grid per kernel index
   std::vector<long long> goff;        // offset (double2) of scale j's G block in Gs
-  DevBuf f, Gtop, Gs, scratch;
+  DevBuf f, Gtop, Gs, Gr, scratch;  // Gr: MW resampling target (one scale at a time)
   SynthCfg syn_top, syn_scales;
   AnaCfg ana_top, ana_scales;
   double2* bufs() const { return nullptr; }
@@ -1053,6 +1113,9 @@ int s2w_wav_plan_create(int scheme, int L, int batch, int is_real, int n_kern,
   if ((r = p->Gtop.ensure(sizeof(double2) * (size_t)batch * p->top->n_bins(cplx) * L)) != S2W_OK)
     return bail(r);
   if ((r = p->Gs.ensure(sizeof(double2) * (size_t)off)) != S2W_OK) return bail(r);
+  if (p->top->syn_on_ana() &&
+      (r = p->Gr.ensure(sizeof(double2) * (size_t)batch * p->top->n_bins(cplx) * L)) != S2W_OK)
+    return bail(r);
   if ((r = p->scratch.ensure(sizeof(double2) * fft_split_scratch_elems(p->top->logM))) != S2W_OK)
     return bail(r);
 
@@ -1204,7 +1267,7 @@ int s2w_wav_analysis_pixel(s2w_wav_plan* p, const double* map, double* const* sc
   CHECK(run_synth(p->syn_scales, p->top->seed_c, bufs, st));
   for (int j = 0; j < p->nk; ++j)
     CHECK(inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
-                        p->scratch.as<double2>(), st));
+                        p->scratch.as<double2>(), p->Gr.as<double2>(), st));
   return S2W_OK;
 }
 
@@ -1227,7 +1290,7 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, do
   // sh_synthesis at L (transform.py:200)
   CHECK(run_synth(p->syn_top, p->top->seed_c, bufs, st));
   CHECK(inverse_rings(p->top, p->B, !cplx, p->Gtop.as<double2>(), map, p->scratch.as<double2>(),
-                      st));
+                      p->Gr.as<double2>(), st));
   return S2W_OK;
 }
 
@@ -1297,8 +1360,8 @@ int s2w_test_rings_inverse(int scheme, int L, int n_sets, int is_real, const dou
   GridRes* g;
   CHECK(get_grid(dev, scheme, L, &g));
   CHECK(g_test_scratch.ensure(sizeof(double2) * fft_split_scratch_elems(g->logM)));
-  return inverse_rings(g, n_sets, is_real != 0, (const double2*)G, map,
-                       g_test_scratch.as<double2>(), (cudaStream_t)stream);
+  return phi_inverse(g, n_sets, is_real != 0, (const double2*)G, map,
+                     g_test_scratch.as<double2>(), (cudaStream_t)stream);
 }
 
 int s2w_test_rings_forward(int scheme, int L, int n_sets, int is_real, int theta_stage,

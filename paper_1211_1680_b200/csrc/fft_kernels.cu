@@ -306,6 +306,109 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- MW synthesis theta stage
+// Resampling of a pair (even m, odd m) of columns from the analysis rings
+// theta''_j = (2j+1) pi / N2 (N2 = 2k, symmetric, where the Legendre synthesis
+// ran) to the MW rings theta_t = (2t+1) pi / N: parity extension to the full
+// circle (2 pi - theta''_j = theta''_{N2-1-j}), DFT_N2 -> Fourier coefficients
+// b_q (|q| < k, exact: G is a trig polynomial of degree k-1), inverse DFT_N at
+// the MW points, parity split via theta_{N-1-t} = 2 pi - theta_t.
+S2W_DEV double2 theta_syn_ext(const double2* ge, const double2* go, int n, int k) {
+  const bool lo = n < k;
+  const int src = lo ? n : 2 * k - 1 - n;
+  const double2 e = ge ? __ldg(&ge[src]) : make_double2(0.0, 0.0);
+  const double2 o = go ? __ldg(&go[src]) : make_double2(0.0, 0.0);
+  return lo ? cadd(e, o) : csub(e, o);
+}
+
+struct ThetaSynRow {
+  const double2 *ge, *go;
+  double2* out;
+  int ce, co;  // output columns (-1: none)
+};
+
+S2W_DEV ThetaSynRow theta_syn_row(const ThetaSynArgs& a, int row, bool valid) {
+  ThetaSynRow R{nullptr, nullptr, nullptr, -1, -1};
+  if (!valid) return R;
+  const int set = row / a.n_pairs, pi = row - set * a.n_pairs;
+  const int2 pr = a.pairs[pi];
+  const size_t base = (size_t)set * a.n_bins;
+  if (pr.x >= 0) R.ge = a.in + (base + pr.x) * a.k;
+  if (pr.y >= 0) R.go = a.in + (base + pr.y) * a.k;
+  R.out = a.out + (size_t)set * a.k * a.n_bins;
+  R.ce = pr.x;
+  R.co = pr.y;
+  return R;
+}
+
+S2W_DEV void theta_syn_store(const ThetaSynRow& R, const ThetaSynArgs& a, int t, double2 wt,
+                             double2 wr) {
+  if (R.ce >= 0) R.out[(size_t)t * a.n_bins + R.ce] = cscale(cadd(wt, wr), 0.5);
+  if (R.co >= 0) R.out[(size_t)t * a.n_bins + R.co] = cscale(csub(wt, wr), 0.5);
+}
+
+template <int LOGM>
+__global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
+  const int N = T.N, N2 = T.N2, k = a.k;
+  const int grp = threadIdx.x / GS, gtid = threadIdx.x % GS;
+  double2* buf = smem + (size_t)grp * M;
+  double2* tw = smem + (size_t)a.rpc * M;
+  load_tw<LOGM>(tw, T.tw);
+  const int row = blockIdx.x * a.rpc + grp;
+  const bool valid = row < a.n_sets * a.n_pairs;
+  const ThetaSynRow R = theta_syn_row(a, row, valid);
+
+  // 1. parity extension on the 2k analysis points, times the chirp c2
+  for (int n0 = gtid; n0 < M; n0 += 8 * GS) {
+    double2 x[8], c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * GS;
+      const bool in = valid && n < N2;
+      x[u] = in ? theta_syn_ext(R.ge, R.go, n, k) : make_double2(0.0, 0.0);
+      c[u] = in ? __ldg(&T.chirp2[n]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u * GS;
+      if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
+    }
+  }
+  __syncthreads();
+  // 2. DFT_N2 (Bluestein)
+  fft_conv<LOGM, GS>(buf, tw, T.bl_fwd2, gtid);
+  // 3. inverse-DFT_N input X_n = DFT_N2[src(n)] ph4[n]; src = n (n < k) or
+  //    n + 1 (= N2 + n - N, n >= k): overlapping moves, so all values are read
+  //    into registers first (N <= 8 GS)
+  double2 xv[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int n = gtid + u * GS;
+    xv[u] = make_double2(0.0, 0.0);
+    if (n < N) xv[u] = cmul(buf[swz(n < k ? n : n + 1)], __ldg(&T.ph4[n]));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int n = gtid + u * GS;
+    if (n < N) buf[swz(n)] = xv[u];
+  }
+  for (int n = N + gtid; n < M; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 4. inverse DFT_N (Bluestein) at the MW points; rings t and N-1-t
+  fft_conv<LOGM, GS>(buf, tw, T.bl_inv, gtid);
+  if (!valid) return;
+  for (int t = gtid; t < k; t += GS) {
+    const int tr = N - 1 - t;
+    const double2 wt = cmulc(buf[swz(t)], __ldg(&T.chirp[t]));
+    const double2 wr = cmulc(buf[swz(tr)], __ldg(&T.chirp[tr]));
+    theta_syn_store(R, a, t, wt, wr);
+  }
+}
+
 // =====================================================================
 // Split mode for M > 8192 (L > 2048): the length-M cyclic convolution is
 // done as two shared-memory FFT pairs of length F = M/2 (DIF first stage
@@ -531,6 +634,59 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
   }
 }
 
+template <int LOGF>
+__global__ void __launch_bounds__(SPLIT_T) theta_syn_split_kernel(ThetaSynArgs a) {
+  extern __shared__ double2 smem[];
+  const FftTablesDev& T = a.T;
+  constexpr int logM = LOGF + 1, F = 1 << LOGF;
+  const int N = T.N, N2 = T.N2, k = a.k;
+  double2* buf = smem;
+  double2* twF = smem + F;
+  double2* octM = twF + ((fft_ntw(LOGF) + 7) & ~7);
+  load_tw<LOGF>(twF, T.tw);
+  load_octant(octM, T.octM, logM);
+  double2* u = a.scratch + (size_t)blockIdx.x * 2 * F;  // even-half results
+  double2* sv = u + F;                                 // saved row (X_n)
+  const int n_rows = a.n_sets * a.n_pairs;
+  __syncthreads();
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const ThetaSynRow R = theta_syn_row(a, row, true);
+    // 1-2. DFT_N2 of the parity extension (Bluestein)
+    split_conv<LOGF>(buf, u, T.bl_fwd2, twF, [&](int half) {
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N2) {
+          v = cmul(theta_syn_ext(R.ge, R.go, n, k), __ldg(&T.chirp2[n]));
+          if (half) v = cmul(v, wM(n, octM, logM));
+        }
+        buf[swz(n)] = v;
+      }
+    });
+    // 3. X_n = DFT_N2[src(n)] ph4[n]  (src < N2 <= F: the first output half)
+    for (int n = threadIdx.x; n < N; n += SPLIT_T) {
+      const int src = n < k ? n : n + 1;
+      const double2 y = cadd(u[src], cmulc(buf[swz(src)], wM(src, octM, logM)));
+      sv[n] = cmul(y, __ldg(&T.ph4[n]));
+    }
+    __syncthreads();
+    // 4. inverse DFT_N (Bluestein); rings t and N-1-t
+    split_conv<LOGF>(buf, u, T.bl_inv, twF, [&](int half) {
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) {
+        double2 v = (n < N) ? sv[n] : make_double2(0.0, 0.0);
+        if (half && n < N) v = cmul(v, wM(n, octM, logM));
+        buf[swz(n)] = v;
+      }
+    });
+    for (int t = threadIdx.x; t < k; t += SPLIT_T) {
+      const int tr = N - 1 - t;
+      const double2 zt = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
+      const double2 zr = cadd(u[tr], cmulc(buf[swz(tr)], wM(tr, octM, logM)));
+      theta_syn_store(R, a, t, cmulc(zt, __ldg(&T.chirp[t])), cmulc(zr, __ldg(&T.chirp[tr])));
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static cudaError_t set_smem(const void* fn, size_t smem) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -647,6 +803,12 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
   pairs.resize(n);
   for (size_t i = 0; i < n; ++i)
     pairs[i] = make_int2(i < ev.size() ? ev[i] : -1, i < od.size() ? od[i] : -1);
+}
+
+cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
+  const int n_rows = a.n_sets * a.n_pairs;
+  if (n_rows == 0) return cudaSuccess;
+  S2W_FFT_DISPATCH(theta_syn_kernel, theta_syn_split_kernel, a, n_rows, st)
 }
 
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {

@@ -25,6 +25,9 @@ struct FftTablesDev {
   const double2* chirp2;  // [N2] c2_n = exp(-i pi n^2/N2)
   const double2* bl_ev;   // [M]  FFT(c2, circular)/M
   const double2* ph2;     // [N2] exp(i pi q(n)/N2) conj(c2_n), q(n) = n or n - N2 (|q| < k)
+  // MW synthesis resampling (analysis rings -> sampling rings, theta_syn_kernel):
+  const double2* bl_fwd2; // [M]  FFT(conj c2, circular)/M   (forward DFT_N2)
+  const double2* ph4;     // [N]  c2_src e^{-i pi q/N2} e^{i pi q/N} conj(c_n) / N2, q = n or n - N
 };
 
 struct PhiFwdArgs {
@@ -64,7 +67,21 @@ struct ThetaArgs {
   double2* scratch;
 };
 
+// MW synthesis theta stage: G on the analysis rings theta''_j (m-major) ->
+// G on the MW rings (ring-major), order pairs by parity as in ThetaArgs.
+struct ThetaSynArgs {
+  FftTablesDev T;
+  int n_sets, k, n_bins;  // n_bins = columns per set
+  const int2* pairs;
+  int n_pairs;
+  const double2* in;  // [set][mi][k]  (analysis rings)
+  double2* out;       // [set][t][n_bins] (MW rings), must not alias in
+  int rpc;
+  double2* scratch;
+};
+
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
+cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st);
 // Scratch (double2 elements) the split-mode kernels need for convolution size 2^logM.
 size_t fft_split_scratch_elems(int logM);
 // Length of the pass-twiddle table of the FFT engine of size 2^logE.
@@ -86,6 +103,7 @@ struct LegGridDev {
   const int2* act;       // [k] active ring range [lo, hi) per order m
   const int* binmap;     // bin -> local column (synthesis) / row (analysis); nullptr = identity
   int n_cols;            // synthesis output row stride (n_bins unless sharded by order)
+  int mmajor;            // synthesis output m-major [col][t] (else ring-major [t][col])
 };
 
 // Buffers are addressed as (slot, element offset) into the per-launch base
@@ -132,6 +150,7 @@ struct LegSynthArgs {
   int cplx;
   int ns;  // compile-time set width selected by the launcher
   int win; // degrees per shared-memory window (leg_synth_window)
+  int sym; // every grid is equator-symmetric (LegGridDev::n_north > 0)
   double2* bufs[S2W_NBUF];
 };
 
