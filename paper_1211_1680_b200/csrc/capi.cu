@@ -8,6 +8,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -339,7 +340,7 @@ struct GridRes {
   RingSet syn, ana;
   double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr,
-          *bl_fwd2 = nullptr, *ph4 = nullptr;
+          *bl_fwd2 = nullptr, *ph4 = nullptr, *ph2d = nullptr, *ph4d = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
   int2 *pairs_r = nullptr, *pairs_c = nullptr;
@@ -374,11 +375,23 @@ struct GridRes {
     t.bl_ev = bl_ev;
     t.bl_fwd2 = bl_fwd2;
     t.ph4 = ph4;
+    t.ph2d = ph2d;
+    t.ph4d = ph4d;
     return t;
   }
   // MW synthesis runs on the (symmetric) analysis rings and is resampled to
   // the MW rings by theta_syn_kernel; GL synthesis runs on its own rings.
-  bool syn_on_ana() const { return scheme == S2W_SCHEME_MW; }
+  // Small MW grids synthesise on their own rings directly: there the
+  // resampling (O(k^2 log k)) costs more than the halved recursion saves.
+  bool syn_on_ana() const { return scheme == S2W_SCHEME_MW && k >= syn_resample_min(); }
+  static int syn_resample_min() {
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("S2W_SYN_RESAMPLE_MIN");
+      v = e ? atoi(e) : 1024;
+    }
+    return v;
+  }
   LegGridDev leg(bool cplx, bool analysis) const {
     const RingSet& rs = (analysis || syn_on_ana()) ? ana : syn;
     LegGridDev g;
@@ -579,13 +592,21 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     if (n > 0) b2[M - n] = std::conj(c2[n]);
   }
   // synthesis resampling: X_n = DFT_N2[src] ph4[n], n < N (see theta_syn_kernel)
-  std::vector<double2> ph4(N);
+  std::vector<double2> ph4(N), ph4d(N), ph2d(N2);
   for (int n = 0; n < N; ++n) {
     const int q = n < k ? n : n - N;
     const int src = q >= 0 ? q : N2 + q;
     const ld a2 = -PI_L * (ld)q / (ld)N2, a1 = PI_L * (ld)q / (ld)N;
-    ph4[n] = d2(c2[src] * cld(std::cos(a2), std::sin(a2)) * cld(std::cos(a1), std::sin(a1)) *
-                std::conj(cl[n]) / (ld)N2);
+    const cld base = cld(std::cos(a2), std::sin(a2)) * cld(std::cos(a1), std::sin(a1)) *
+                     std::conj(cl[n]) / (ld)N2;
+    ph4[n] = d2(c2[src] * base);
+    ph4d[n] = d2(base);
+  }
+  for (int n = 0; n < N2; ++n) {
+    const int q = n < k ? n : n - N2;
+    const ld a2 = -PI_L * (ld)q / (ld)N2;
+    ph2d[n] = (n >= k && n <= N2 - k) ? make_double2(0.0, 0.0)
+                                      : d2(cld(std::cos(a2), std::sin(a2)));
   }
   for (int n = 0; n < N2; ++n) {
     const int q = n < k ? n : n - N2;
@@ -608,6 +629,8 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->bl_ev, spectrum_brev(cc2)));
   CHECK(upload_new(&g->bl_fwd2, spectrum_brev(b2)));
   CHECK(upload_new(&g->ph4, ph4));
+  CHECK(upload_new(&g->ph2d, ph2d));
+  CHECK(upload_new(&g->ph4d, ph4d));
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   g_grids[key] = g;
   *out = g;
@@ -652,8 +675,9 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   std::vector<It> items;
   int maxn = 1;
   for (auto& gr : groups) maxn = std::max<int>(maxn, (int)gr.sets.size());
-  cfg.sym = 1;
-  for (auto& gr : groups) cfg.sym &= gr.g->leg(cplx, false).n_north > 0 ? 1 : 0;
+  // the symmetric kernel also runs asymmetric grids (n_north == 0) as such
+  cfg.sym = 0;
+  for (auto& gr : groups) cfg.sym |= gr.g->leg(cplx, false).n_north > 0 ? 1 : 0;
   // symmetric rings keep two accumulator sets: at most 4 complex / 8 real sets per CTA
   const int ns = cfg.sym ? std::min(pick_ns(maxn, cplx), cplx ? 4 : 8) : pick_ns(maxn, cplx);
   for (size_t gi = 0; gi < groups.size(); ++gi) {

@@ -129,7 +129,9 @@ S2W_DEV void powers16(double2* w, double2 u) {
 }
 
 // One radix-16 pass at span 2^LS (forward DIF, or its adjoint when INV).
-template <int LOGM, int GS, int LS, bool INV>
+// TWS: stride into the twiddle table (2 when a half-size transform borrows
+// the table of the engine size: W_{16s}^j = W_{32s}^{2j}).
+template <int LOGM, int GS, int LS, bool INV, int TWS = 1>
 S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, int gtid) {
   constexpr int NB = (1 << LOGM) / 16;
   constexpr int S = 1 << LS;
@@ -143,7 +145,7 @@ S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, i
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = buf[sb ^ swz(k << LS)];
     double2 w[16];
-    powers16(w, tw[j]);
+    powers16(w, tw[j * TWS]);
     if constexpr (!INV) {
       dif<4>(v);
 #pragma unroll
@@ -184,12 +186,15 @@ S2W_DEV void conv_core(double2* __restrict__ buf, const double2* __restrict__ ta
   }
 }
 
-template <int LOGM, int GS, int P>
+// tw: table of the size 2^(LOGM + TWSH) (TWSH = 0 or 1), i.e. for a
+// half-size transform the engine's own table read at stride 2.
+template <int LOGM, int GS, int P, int TWSH = 0>
 S2W_DEV void fwd_passes(double2* buf, const double2* tw, int gtid) {
   if constexpr (P < fft_k16(LOGM)) {
-    pass16<LOGM, GS, LOGM - 4 * (P + 1), false>(buf, tw + fft_tw_off(LOGM, P), gtid);
+    pass16<LOGM, GS, LOGM - 4 * (P + 1), false, 1 << TWSH>(
+        buf, tw + fft_tw_off(LOGM + TWSH, P), gtid);
     __syncthreads();
-    fwd_passes<LOGM, GS, P + 1>(buf, tw, gtid);
+    fwd_passes<LOGM, GS, P + 1, TWSH>(buf, tw, gtid);
   }
 }
 template <int LOGM, int GS, int P>
@@ -200,6 +205,39 @@ S2W_DEV void inv_passes(double2* buf, const double2* tw, int gtid) {
     inv_passes<LOGM, GS, P - 1>(buf, tw, gtid);
   }
 }
+
+// Last forward pass alone (radix 2^CB at span 1, no product).
+template <int LOGM, int GS>
+S2W_DEV void fwd_core(double2* __restrict__ buf, int gtid) {
+  constexpr int CB = LOGM - 4 * fft_k16(LOGM);
+  constexpr int R = 1 << CB;
+  constexpr int NB = (1 << LOGM) / R;
+#pragma unroll
+  for (int it = 0; it < (NB + GS - 1) / GS; ++it) {
+    const int b = gtid + it * GS;
+    if (NB % GS != 0 && b >= NB) break;
+    const int sb = swz(b * R);
+    double2 v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];
+    dif<CB>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[sb ^ swz(i)] = v[i];
+  }
+}
+
+// Forward DFT of the first 2^LOGN elements (natural order in, bit-reversed
+// order out: X_q at swz(fft_brev<LOGN>(q))), unnormalised.  TWSH as in
+// fwd_passes.  Precondition: row written and synced.  Ends synced.
+template <int LOGN, int GS, int TWSH>
+S2W_DEV void fft_fwd(double2* buf, const double2* tw, int gtid) {
+  fwd_passes<LOGN, GS, 0, TWSH>(buf, tw, gtid);
+  fwd_core<LOGN, GS>(buf, gtid);
+  __syncthreads();
+}
+
+template <int LOGN>
+S2W_DEV int fft_brev(int q) { return (int)(__brev((unsigned)q) >> (32 - LOGN)); }
 
 // Cyclic convolution of the row with the table's sequence: forward FFT,
 // product, inverse FFT.  tw: the pass twiddles (fft_ntw(LOGM) entries,

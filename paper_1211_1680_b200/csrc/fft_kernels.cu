@@ -274,24 +274,41 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
   //    Bluestein input X_n = H'(q) e^{i pi q/N2} conj(c2_n), n = q mod N2.
   //    H'(q) sits at q (q >= 0) and M + q (q < 0); the moves read [M-k+1, M)
   //    and write [k, N2), disjoint.
+  //    When N2 = M/2 (k a power of two) the inverse DFT_N2 is a direct
+  //    half-size FFT instead: w = conj(DFT_N2(conj X')), X'_n = H'(q) e^{i pi q/N2}.
   const int N2 = T.N2;
+  const bool pow2 = 2 * N2 == M;
+  const double2* phs = pow2 ? T.ph2d : T.ph2;
   for (int n0 = gtid; n0 < N2; n0 += 8 * GS) {
     double2 ph[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int n = n0 + u * GS;
-      ph[u] = (n < N2) ? __ldg(&T.ph2[n]) : make_double2(0.0, 0.0);
+      ph[u] = (n < N2) ? __ldg(&phs[n]) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int n = n0 + u * GS;
       if (n >= N2) continue;
-      const double2 v = (n < k) ? buf[swz(n)]
-                                : (n > N2 - k ? buf[swz(M - N2 + n)] : make_double2(0.0, 0.0));
+      double2 v = (n < k) ? buf[swz(n)]
+                          : (n > N2 - k ? buf[swz(M - N2 + n)] : make_double2(0.0, 0.0));
+      if (pow2) v = cconj(v);
       buf[swz(n)] = cmul(v, ph[u]);
     }
   }
   __syncthreads();
+  if (pow2) {
+    // 6. direct FFT of length N2 = M/2; rings j and N2-1-j, split by parity
+    fft_fwd<LOGM - 1, GS, 1>(buf, tw, gtid);
+    if (!valid) return;
+    for (int t = gtid; t < k; t += GS) {
+      const int tr = N2 - 1 - t;
+      const double2 wt = cconj(buf[swz(fft_brev<LOGM - 1>(t))]);
+      const double2 wr = cconj(buf[swz(fft_brev<LOGM - 1>(tr))]);
+      theta_store(P, a, t, wt, wr);
+    }
+    return;
+  }
   for (int n = N2 + gtid; n < M; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 6. inverse DFT_N2 (Bluestein); rings j and N2-1-j (its mirror 2 pi - theta''_j),
@@ -361,7 +378,9 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArg
   const bool valid = row < a.n_sets * a.n_pairs;
   const ThetaSynRow R = theta_syn_row(a, row, valid);
 
-  // 1. parity extension on the 2k analysis points, times the chirp c2
+  // 1. parity extension on the 2k analysis points (times the chirp c2 unless
+  //    N2 = M/2, where the DFT_N2 is a direct half-size FFT)
+  const bool pow2 = 2 * N2 == M;
   for (int n0 = gtid; n0 < M; n0 += 8 * GS) {
     double2 x[8], c[8];
 #pragma unroll
@@ -369,7 +388,7 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArg
       const int n = n0 + u * GS;
       const bool in = valid && n < N2;
       x[u] = in ? theta_syn_ext(R.ge, R.go, n, k) : make_double2(0.0, 0.0);
-      c[u] = in ? __ldg(&T.chirp2[n]) : make_double2(0.0, 0.0);
+      c[u] = in ? (pow2 ? make_double2(1.0, 0.0) : __ldg(&T.chirp2[n])) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -378,8 +397,9 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArg
     }
   }
   __syncthreads();
-  // 2. DFT_N2 (Bluestein)
-  fft_conv<LOGM, GS>(buf, tw, T.bl_fwd2, gtid);
+  // 2. DFT_N2 (Bluestein, or direct)
+  if (pow2) fft_fwd<LOGM - 1, GS, 1>(buf, tw, gtid);
+  else fft_conv<LOGM, GS>(buf, tw, T.bl_fwd2, gtid);
   // 3. inverse-DFT_N input X_n = DFT_N2[src(n)] ph4[n]; src = n (n < k) or
   //    n + 1 (= N2 + n - N, n >= k): overlapping moves, so all values are read
   //    into registers first (N <= 8 GS)
@@ -388,7 +408,11 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArg
   for (int u = 0; u < 8; ++u) {
     const int n = gtid + u * GS;
     xv[u] = make_double2(0.0, 0.0);
-    if (n < N) xv[u] = cmul(buf[swz(n < k ? n : n + 1)], __ldg(&T.ph4[n]));
+    if (n < N) {
+      const int src = n < k ? n : n + 1;
+      xv[u] = pow2 ? cmul(buf[swz(fft_brev<LOGM - 1>(src))], __ldg(&T.ph4d[n]))
+                   : cmul(buf[swz(src)], __ldg(&T.ph4[n]));
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -613,9 +637,21 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
         const int j = F + n - N2;  // position M + q = j + F
         h = csub(u[j], cmulc(buf[swz(j)], wM(j, octM, logM)));
       }
-      sv[n] = cmul(h, __ldg(&T.ph2[n]));
+      sv[n] = (N2 == F) ? cmul(cconj(h), __ldg(&T.ph2d[n])) : cmul(h, __ldg(&T.ph2[n]));
     }
     __syncthreads();
+    if (2 * N2 == 2 * F) {
+      // 6. N2 = F (k a power of two): direct FFT of the engine size,
+      //    w = conj(DFT(conj X')), X'_n = X_n / conj(c2_n) stored by step 5 via ph2d
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) buf[swz(n)] = sv[n];
+      __syncthreads();
+      fft_fwd<LOGF, SPLIT_T, 0>(buf, twF, threadIdx.x);
+      for (int t = threadIdx.x; t < k; t += SPLIT_T) {
+        const int tr = N2 - 1 - t;
+        theta_store(P, a, t, cconj(buf[swz(fft_brev<LOGF>(t))]),
+                    cconj(buf[swz(fft_brev<LOGF>(tr))]));
+      }
+    } else {
     // 6. inverse DFT_N2 (Bluestein); rings t and N2-1-t, split by parity
     split_conv<LOGF>(buf, u, T.bl_ev, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
@@ -629,6 +665,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_split_kernel(ThetaArgs a) {
       const double2 zt = cadd(u[t], cmulc(buf[swz(t)], wM(t, octM, logM)));
       const double2 zr = cadd(u[tr], cmulc(buf[swz(tr)], wM(tr, octM, logM)));
       theta_store(P, a, t, cmulc(zt, __ldg(&T.chirp2[t])), cmulc(zr, __ldg(&T.chirp2[tr])));
+    }
     }
     __syncthreads();
   }
@@ -651,6 +688,18 @@ __global__ void __launch_bounds__(SPLIT_T) theta_syn_split_kernel(ThetaSynArgs a
   __syncthreads();
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
     const ThetaSynRow R = theta_syn_row(a, row, true);
+    if (N2 == F) {
+      // 1-2. N2 = F (k a power of two): direct FFT of the engine size
+      for (int n = threadIdx.x; n < F; n += SPLIT_T) buf[swz(n)] = theta_syn_ext(R.ge, R.go, n, k);
+      __syncthreads();
+      fft_fwd<LOGF, SPLIT_T, 0>(buf, twF, threadIdx.x);
+      // 3. X_n = DFT_N2[src(n)] ph4d[n]
+      for (int n = threadIdx.x; n < N; n += SPLIT_T) {
+        const int src = n < k ? n : n + 1;
+        sv[n] = cmul(buf[swz(fft_brev<LOGF>(src))], __ldg(&T.ph4d[n]));
+      }
+      __syncthreads();
+    } else {
     // 1-2. DFT_N2 of the parity extension (Bluestein)
     split_conv<LOGF>(buf, u, T.bl_fwd2, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {
@@ -669,6 +718,7 @@ __global__ void __launch_bounds__(SPLIT_T) theta_syn_split_kernel(ThetaSynArgs a
       sv[n] = cmul(y, __ldg(&T.ph4[n]));
     }
     __syncthreads();
+    }
     // 4. inverse DFT_N (Bluestein); rings t and N-1-t
     split_conv<LOGF>(buf, u, T.bl_inv, twF, [&](int half) {
       for (int n = threadIdx.x; n < F; n += SPLIT_T) {

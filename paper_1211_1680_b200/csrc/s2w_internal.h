@@ -28,6 +28,9 @@ struct FftTablesDev {
   // MW synthesis resampling (analysis rings -> sampling rings, theta_syn_kernel):
   const double2* bl_fwd2; // [M]  FFT(conj c2, circular)/M   (forward DFT_N2)
   const double2* ph4;     // [N]  c2_src e^{-i pi q/N2} e^{i pi q/N} conj(c_n) / N2, q = n or n - N
+  // N2 = M/2 (k a power of two; the DFT_N2 steps are direct half-size FFTs):
+  const double2* ph2d;    // [N2] exp(-i pi q(n)/N2)  (conjugated evaluation input)
+  const double2* ph4d;    // [N]  e^{-i pi q/N2} e^{i pi q/N} conj(c_n) / N2
 };
 
 struct PhiFwdArgs {
