@@ -14,7 +14,8 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+             "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in data:
         name = r[ki].split("(")[0].split("<")[0].replace("void ", "").strip()
