@@ -15,6 +15,9 @@
  *   s2w_wav_synthesis_harmonic<- transform.py:153-172 (wav_synthesis_harmonic)
  *   s2w_wav_analysis_pixel    <- transform.py:175-191 (wav_analysis_pixel)
  *   s2w_wav_synthesis_pixel   <- transform.py:194-202 (wav_synthesis_pixel)
+ *   s2w_wav_analysis_pixel_threshold, s2w_wav_denoise_pixel
+ *                             <- denoise.py:78-103 (hard_threshold / denoise_pipeline),
+ *                                threshold fused into the scale maps' ring-DFT epilogue
  *
  * Conventions ("contiguous 64-bit float buffers plus scalar
  * parameters; no object graphs cross the boundary"):
@@ -114,6 +117,18 @@ int s2w_wav_analysis_pixel(s2w_wav_plan* plan, const double* map, double* const*
 /* scale_maps[j] -> map (exact inverse of s2w_wav_analysis_pixel). */
 int s2w_wav_synthesis_pixel(s2w_wav_plan* plan, const double* const* scale_maps, double* map,
                             void* stream);
+
+/* Wavelet analysis with the denoiser's hard threshold fused in (denoise.py:78-96):
+ * samples of wavelet map j (1 <= j < n_kern) with |value| < thresholds[j] are
+ * zeroed as they are written; the scaling map (j = 0, thresholds[0] ignored)
+ * passes unchanged.  thresholds: HOST array of n_kern doubles, each >= 0. */
+int s2w_wav_analysis_pixel_threshold(s2w_wav_plan* plan, const double* map,
+                                     const double* thresholds, double* const* scale_maps,
+                                     void* stream);
+/* denoise_pipeline (denoise.py:99-103): thresholded analysis into the caller's
+ * scale_maps workspace, then wavelet synthesis into map_out. */
+int s2w_wav_denoise_pixel(s2w_wav_plan* plan, const double* map, const double* thresholds,
+                          double* const* scale_maps, double* map_out, void* stream);
 
 /* Coefficient workspace of the plan (batch*L*L complex, device): after
  * s2w_wav_analysis_pixel it holds f_lm of the input map; after

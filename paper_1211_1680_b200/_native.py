@@ -41,6 +41,10 @@ _PROTOS = {
     "s2w_wav_synthesis_harmonic": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_wav_analysis_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "s2w_wav_synthesis_pixel": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_wav_analysis_pixel_threshold": (_c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_double),
+                                                  ctypes.POINTER(_vp), _vp]),
+    "s2w_wav_denoise_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_shard_plan_create": (
         _c_int,
         [_c_int, _c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int), _c_int, _c_int, _c_int,

@@ -893,8 +893,9 @@ static int theta_resample(const GridRes* g, int n_sets, bool real, const double2
 
 // Ring-major G on the sampling rings -> maps (ring DFTs, MW pole pin).
 static int phi_inverse(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
-                       double2* scratch, cudaStream_t st) {
+                       double2* scratch, cudaStream_t st, double thresh = 0.0) {
   PhiInvArgs pa;
+  pa.thresh = thresh;
   pa.scratch = scratch;
   pa.T = g->fft();
   pa.n_sets = n_sets;
@@ -913,12 +914,12 @@ static int phi_inverse(const GridRes* g, int n_sets, bool real, const double2* G
 // Legendre synthesis output G -> maps.  MW: G is m-major on the analysis
 // rings and is first resampled into tmp (ring-major, MW rings).
 static int inverse_rings(const GridRes* g, int n_sets, bool real, const double2* G, double* map,
-                         double2* scratch, double2* tmp, cudaStream_t st) {
+                         double2* scratch, double2* tmp, cudaStream_t st, double thresh = 0.0) {
   if (g->syn_on_ana()) {
     CHECK(theta_resample(g, n_sets, real, G, tmp, scratch, st));
     G = tmp;
   }
-  return phi_inverse(g, n_sets, real, G, map, scratch, st);
+  return phi_inverse(g, n_sets, real, G, map, scratch, st, thresh);
 }
 
 // ------------------------------------------------------------------ SHT plan
@@ -1273,9 +1274,33 @@ int s2w_wav_synthesis_harmonic(s2w_wav_plan* p, int full_band, const double* con
   return S2W_OK;
 }
 
+static int wav_analysis_pixel_impl(s2w_wav_plan* p, const double* map, const double* thresholds,
+                                   double* const* scale_maps, void* stream);
+
 int s2w_wav_analysis_pixel(s2w_wav_plan* p, const double* map, double* const* scale_maps,
                            void* stream) {
+  return wav_analysis_pixel_impl(p, map, nullptr, scale_maps, stream);
+}
+
+int s2w_wav_analysis_pixel_threshold(s2w_wav_plan* p, const double* map, const double* thresholds,
+                                     double* const* scale_maps, void* stream) {
+  if (!thresholds) return fail(S2W_EPARAM, "null threshold table");
+  return wav_analysis_pixel_impl(p, map, thresholds, scale_maps, stream);
+}
+
+int s2w_wav_denoise_pixel(s2w_wav_plan* p, const double* map, const double* thresholds,
+                          double* const* scale_maps, double* map_out, void* stream) {
+  if (!thresholds || !map_out) return fail(S2W_EPARAM, "null argument");
+  CHECK(wav_analysis_pixel_impl(p, map, thresholds, scale_maps, stream));
+  return s2w_wav_synthesis_pixel(p, (const double* const*)scale_maps, map_out, stream);
+}
+
+static int wav_analysis_pixel_impl(s2w_wav_plan* p, const double* map, const double* thresholds,
+                                   double* const* scale_maps, void* stream) {
   if (!p || !map || !scale_maps) return fail(S2W_EPARAM, "null argument");
+  if (thresholds)
+    for (int j = 1; j < p->nk; ++j)
+      if (!(thresholds[j] >= 0.0)) return fail(S2W_EPARAM, "threshold %d must be >= 0", j);
   DeviceGuard dg(p->device);
   CU(dg.err);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1289,9 +1314,12 @@ int s2w_wav_analysis_pixel(s2w_wav_plan* p, const double* map, double* const* sc
   CHECK(run_ana(p->ana_top, p->top->seed_c, bufs, st));
   // tiling + truncation fused into the grouped per-scale synthesis (transform.py:187-190)
   CHECK(run_synth(p->syn_scales, p->top->seed_c, bufs, st));
+  // hard thresholding of the wavelet maps (not the scaling map) fused into
+  // the ring-DFT epilogue (denoise.py:78-96)
   for (int j = 0; j < p->nk; ++j)
     CHECK(inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
-                        p->scratch.as<double2>(), p->Gr.as<double2>(), st));
+                        p->scratch.as<double2>(), p->Gr.as<double2>(), st,
+                        (thresholds && j > 0) ? thresholds[j] : 0.0));
   return S2W_OK;
 }
 

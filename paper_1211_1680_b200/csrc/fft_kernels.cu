@@ -29,6 +29,13 @@ __device__ __forceinline__ double2 load_map_elem(const double* __restrict__ in, 
   return __ldg(reinterpret_cast<const double2*>(in) + idx);
 }
 
+// Hard threshold of the denoiser (denoise.py:92): |v| < t -> 0 (t <= 0: no-op;
+// complex magnitudes as np.abs, i.e. hypot).
+S2W_DEV double hard_thresh(double v, double t) { return fabs(v) < t ? 0.0 : v; }
+S2W_DEV double2 hard_thresh(double2 v, double t) {
+  return (t > 0.0 && hypot(v.x, v.y) < t) ? make_double2(0.0, 0.0) : v;
+}
+
 // ---------------------------------------------------------------- phi forward
 template <int LOGM>
 __global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_fwd_kernel(PhiFwdArgs a) {
@@ -156,10 +163,10 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_inv_kernel(PhiInvArgs a)
   for (int q = gtid; q < N; q += GS) {
     const double2 v = cmulc(buf[swz(q)], __ldg(&T.chirp[q]));
     if (a.real) {
-      a.out[ob + q] = pa ? pva.x : v.x;
-      if (vb) a.out[ob + N + q] = pb ? pvb.x : v.y;
+      a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
+      if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
     } else {
-      reinterpret_cast<double2*>(a.out)[ob + q] = pa ? pva : v;
+      reinterpret_cast<double2*>(a.out)[ob + q] = hard_thresh(pa ? pva : v, a.thresh);
     }
   }
 }
@@ -567,10 +574,10 @@ __global__ void __launch_bounds__(SPLIT_T) phi_inv_split_kernel(PhiInvArgs a) {
       const double2 y = cadd(u[q], cmulc(buf[swz(q)], wM(q, octM, logM)));
       const double2 v = cmulc(y, __ldg(&T.chirp[q]));
       if (a.real) {
-        a.out[ob + q] = pa ? pva.x : v.x;
-        if (vb) a.out[ob + N + q] = pb ? pvb.x : v.y;
+        a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
+        if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
       } else {
-        reinterpret_cast<double2*>(a.out)[ob + q] = pa ? pva : v;
+        reinterpret_cast<double2*>(a.out)[ob + q] = hard_thresh(pa ? pva : v, a.thresh);
       }
     }
     __syncthreads();

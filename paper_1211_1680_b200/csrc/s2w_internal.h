@@ -53,6 +53,7 @@ struct PhiInvArgs {
   int n_bins;
   int gsize, rpc;
   double2* scratch;
+  double thresh = 0.0;  // > 0: hard threshold: samples with |value| < thresh are zeroed (denoise)
 };
 
 // The theta operator commutes with the reflection theta -> 2 pi - theta, so an

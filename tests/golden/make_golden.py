@@ -120,6 +120,27 @@ def wavelet_cases():
     np.savez_compressed(OUT / "wavelet.npz", **d)
 
 
+def denoise_cases():
+    """Reference denoise_pipeline (denoise.py:99-103) on a GL map (its only
+    analysable scheme): seeded signal + white noise of harmonic variance sigma^2."""
+    d = {}
+    for name, L, lam, j0, real in (("r32", 32, 2.0, 0, True), ("c24", 24, 2.0, 1, False)):
+        sig = scaled_coeffs(L, 31, real, lambda l: np.where(l >= 2, 1.0 / np.maximum(l * (l + 1), 1), 0.0))
+        noise = sw.gaussian_coeffs(L, np.random.default_rng(32), real_signal=real)
+        sigma = 0.05
+        f = sw.HarmonicCoeffs(L, sig.coeffs + sigma * noise.coeffs, real_signal=real)
+        grid = sw.make_grid(GL, L)
+        noisy = sw.sh_synthesis(f, grid)
+        cfg = sw.TransformConfig(L, lam, j0, scheme=GL, multires=True)
+        model = sw.denoise.make_noise_model(sigma, sw.kernels_for(cfg), 3.0)
+        out = sw.denoise.denoise_pipeline(noisy, sigma, cfg, 3.0)
+        d[f"noisy_{name}"] = noisy.values
+        d[f"sigma_scales_{name}"] = model.sigma_scales
+        d[f"denoised_{name}"] = out.values
+        d[f"params_{name}"] = np.array([L, lam, j0, int(real), sigma])
+    np.savez_compressed(OUT / "denoise.npz", **d)
+
+
 def config_cases():
     """BASELINE configs C1-C3 at full size through the reference (L <= 1024,
     where its recursion is valid): MW synthesis of the seeded inputs, stored as
@@ -144,8 +165,8 @@ def config_cases():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs"]
+    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs", "denoise"]
     for w in which:
         {"sht": sht_cases, "legendre": legendre_cases, "kernels": kernel_cases,
-         "wavelet": wavelet_cases, "configs": config_cases}[w]()
+         "wavelet": wavelet_cases, "configs": config_cases, "denoise": denoise_cases}[w]()
         print("wrote", w)

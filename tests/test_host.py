@@ -153,3 +153,50 @@ def test_error_hierarchy():
     assert issubclass(sw.ParameterError, sw.SphwavError)
     assert issubclass(sw.ParameterError, ValueError)
     assert issubclass(sw.FormatError, sw.SphwavError)
+
+
+# ---------------------------------------------------------------- denoise host logic
+def test_noise_model_matches_reference(golden):
+    g = golden("denoise")
+    for name in ("r32", "c24"):
+        L, lam, j0, real, sigma = g[f"params_{name}"]
+        cfg = sw.TransformConfig(int(L), lam, int(j0), scheme=sw.SamplingScheme.GL, multires=True)
+        model = sw.make_noise_model(sigma, sw.kernels_for(cfg), 3.0)
+        assert np.allclose(model.sigma_scales, g[f"sigma_scales_{name}"], rtol=1e-14, atol=0)
+        assert np.allclose(model.thresholds, 3.0 * g[f"sigma_scales_{name}"], rtol=1e-14, atol=0)
+    with pytest.raises(sw.ParameterError):
+        sw.make_noise_model(-0.1, sw.kernels_for(sw.TransformConfig(16, 2.0, 0)))
+    with pytest.raises(sw.ParameterError):
+        sw.NoiseModel(-1.0, np.zeros(3))
+
+
+def test_snr_db(rng):
+    f = sw.gaussian_coeffs(8, rng)
+    assert sw.snr_db(f, f) == math.inf
+    g = sw.HarmonicCoeffs(8, f.coeffs * 1.1)
+    assert abs(sw.snr_db(f, g) - 20.0) < 1e-9
+    with pytest.raises(sw.ParameterError):
+        sw.snr_db(f, sw.gaussian_coeffs(4, rng))
+    with pytest.raises(sw.ParameterError):
+        sw.snr_db(sw.HarmonicCoeffs(8, np.zeros(64, complex)), f)
+
+
+def test_hard_threshold_host_semantics():
+    cfg = sw.TransformConfig(16, 2.0, 0, scheme=MW)
+    kern = sw.kernels_for(cfg)
+    grids = [sw.make_grid(MW, k) for k in [kern.scaling_bandlimit, *kern.scale_bandlimits]]
+    rng = np.random.default_rng(3)
+    maps = []
+    for g in grids:
+        v = rng.standard_normal(g.sample_shape)
+        v[-1] = v[-1, 0]  # MW pole ring holds one value
+        maps.append(sw.SphereMap(g, v + 0j, is_real=True))
+    dec = sw.WaveletDecomposition(cfg, maps[0], tuple(maps[1:]))
+    model = sw.make_noise_model(0.5, kern, 1.0)
+    out = sw.hard_threshold(dec, model)
+    assert np.array_equal(out.scaling.values, dec.scaling.values)
+    for a, b, t in zip(dec.wavelets, out.wavelets, model.thresholds):
+        assert np.array_equal(b.values, np.where(np.abs(a.values) < t, 0, a.values))
+    bad = sw.NoiseModel(0.5, model.sigma_scales[:-1])
+    with pytest.raises(sw.ParameterError):
+        sw.hard_threshold(dec, bad)
