@@ -15,6 +15,8 @@
  *   s2w_wav_synthesis_harmonic<- transform.py:153-172 (wav_synthesis_harmonic)
  *   s2w_wav_analysis_pixel    <- transform.py:175-191 (wav_analysis_pixel)
  *   s2w_wav_synthesis_pixel   <- transform.py:194-202 (wav_synthesis_pixel)
+ *   s2w_s2wm_read_header, s2w_s2wm_read_payload, s2w_s2wm_write
+ *                             <- mapio.py:83-168 (write_map/read_map/write_flm/read_flm)
  *   s2w_wav_analysis_pixel_threshold, s2w_wav_denoise_pixel
  *                             <- denoise.py:78-103 (hard_threshold / denoise_pipeline),
  *                                threshold fused into the scale maps' ring-DFT epilogue
@@ -47,6 +49,12 @@ extern "C" {
 #define S2W_ECUDA 2     /* CUDA runtime failure                                 */
 #define S2W_ENOMEM 3    /* device allocation failure                            */
 #define S2W_EINTERNAL 4 /* invariant broken inside the library                  */
+/* S2WM files (mapio.py:48-63): FormatError subclasses, and OSError */
+#define S2W_EFORMAT_MAGIC 5     /* NotS2wmFileError        */
+#define S2W_EFORMAT_VERSION 6   /* UnsupportedVersionError */
+#define S2W_EFORMAT_TRUNCATED 7 /* TruncatedFileError      */
+#define S2W_EFORMAT_PAYLOAD 8   /* PayloadMismatchError    */
+#define S2W_EIO 9               /* OSError                 */
 
 #define S2W_SCHEME_GL 0 /* SamplingScheme.GL (grid.py:33-35)                   */
 #define S2W_SCHEME_MW 1 /* SamplingScheme.MW                                   */
@@ -134,6 +142,22 @@ int s2w_wav_denoise_pixel(s2w_wav_plan* plan, const double* map, const double* t
  * s2w_wav_analysis_pixel it holds f_lm of the input map; after
  * s2w_wav_synthesis_pixel the recombined f_lm (transform.py:196-200). */
 int s2w_wav_plan_flm(s2w_wav_plan* plan, double** flm);
+
+/* ---------------------------------------------------------------- S2WM files (mapio.py) */
+/* 22-byte little-endian header (mapio.py:1-15): magic, version, scheme, L, kind, count.
+ * Validates length, magic and version (mapio.py:110-119); the caller checks kind,
+ * scheme, L and count against what it expects (mapio.py:133-145, 163-168). */
+int s2w_s2wm_read_header(const char* path, int* scheme, int* L, int* kind, long long* count);
+/* Payload of `count` float64 (or (re, im) pairs when complex_payload) into dst
+ * (device memory when dst_device, through pinned double-buffered staging on
+ * `stream`, complete on return; else host).  S2W_EFORMAT_TRUNCATED when the file
+ * holds a different number of bytes (mapio.py:122-130). */
+int s2w_s2wm_read_payload(const char* path, long long count, int complex_payload, void* dst,
+                          int dst_device, void* stream);
+/* Header + payload from src (device or host); byte-identical for equal input
+ * (mapio.py:83-106).  kind: 0 real map, 1 complex map, 2 coefficients. */
+int s2w_s2wm_write(const char* path, int scheme, int L, int kind, long long count,
+                   int complex_payload, const void* src, int src_device, void* stream);
 
 /* ---------------------------------------------------------------- shards (multi-GPU) */
 /* One grid restricted to a rank's share of the work: the orders m in `orders`

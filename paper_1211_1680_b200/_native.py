@@ -45,6 +45,13 @@ _PROTOS = {
                                                   ctypes.POINTER(_vp), _vp]),
     "s2w_wav_denoise_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_s2wm_read_header": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_c_int),
+                                      ctypes.POINTER(_c_int), ctypes.POINTER(_c_int),
+                                      ctypes.POINTER(ctypes.c_longlong)]),
+    "s2w_s2wm_read_payload": (_c_int, [ctypes.c_char_p, ctypes.c_longlong, _c_int, _vp, _c_int,
+                                       _vp]),
+    "s2w_s2wm_write": (_c_int, [ctypes.c_char_p, _c_int, _c_int, _c_int, ctypes.c_longlong, _c_int,
+                                _vp, _c_int, _vp]),
     "s2w_shard_plan_create": (
         _c_int,
         [_c_int, _c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int), _c_int, _c_int, _c_int,
@@ -104,9 +111,17 @@ def check(status: int) -> None:
     """Translate a C-ABI status into the reference's exception types."""
     if status == S2W_OK:
         return
+    from . import errors as E
+
     msg = load().s2w_last_error().decode(errors="replace")
     if status == S2W_EPARAM:
         raise ParameterError(msg)
+    fmt = {5: E.NotS2wmFileError, 6: E.UnsupportedVersionError, 7: E.TruncatedFileError,
+           8: E.PayloadMismatchError}
+    if status in fmt:
+        raise fmt[status](msg)
+    if status == 9:
+        raise OSError(msg)
     raise SphwavError(f"s2w status {status}: {msg}")
 
 

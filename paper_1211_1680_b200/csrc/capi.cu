@@ -37,6 +37,17 @@ static int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+// Error reporting for the other translation units (s2wm_io.cu).
+int s2w::io_fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
 #define CU(x)                                                                              \
   do {                                                                                     \
     cudaError_t e_ = (x);                                                                  \

@@ -5,6 +5,9 @@
 
 namespace s2w {
 
+// Set s2w_last_error() and return `code` (capi.cu).
+int io_fail(int code, const char* fmt, ...);
+
 // ------------------------------------------------------------------ FFT tables
 // Per grid band k (N = 2k-1, M = 2^logM >= 2N-1).  All spectra are stored in
 // bit-reversed order (see fft.cuh) and carry the 1/M of the unnormalised

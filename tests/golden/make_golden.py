@@ -141,6 +141,27 @@ def denoise_cases():
     np.savez_compressed(OUT / "denoise.npz", **d)
 
 
+def mapio_cases():
+    """Bytes the reference's own writers produce (mapio.py:83-99)."""
+    import tempfile
+
+    d = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        items = []
+        f = sw.gaussian_coeffs(6, np.random.default_rng(41), real_signal=True)
+        items.append(("gl_real", lambda p: sw.write_map(p, sw.sh_synthesis(f, sw.make_grid(GL, 6)))))
+        g = sw.gaussian_coeffs(5, np.random.default_rng(42), real_signal=False)
+        items.append(("mw_cplx", lambda p: sw.write_map(p, sw.sh_synthesis(g, sw.make_grid(MW, 5)))))
+        items.append(("flm", lambda p: sw.write_flm(p, g)))
+        for name, fn in items:
+            path = Path(tmp) / f"{name}.s2wm"
+            fn(path)
+            d[name] = np.frombuffer(path.read_bytes(), dtype=np.uint8)
+        d["f_gl_real"] = f.coeffs
+        d["f_mw_cplx"] = g.coeffs
+    np.savez_compressed(OUT / "mapio.npz", **d)
+
+
 def config_cases():
     """BASELINE configs C1-C3 at full size through the reference (L <= 1024,
     where its recursion is valid): MW synthesis of the seeded inputs, stored as
@@ -165,8 +186,9 @@ def config_cases():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs", "denoise"]
+    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs", "denoise", "mapio"]
     for w in which:
         {"sht": sht_cases, "legendre": legendre_cases, "kernels": kernel_cases,
-         "wavelet": wavelet_cases, "configs": config_cases, "denoise": denoise_cases}[w]()
+         "wavelet": wavelet_cases, "configs": config_cases, "denoise": denoise_cases,
+         "mapio": mapio_cases}[w]()
         print("wrote", w)
