@@ -106,6 +106,59 @@ class WaveletTransform:
     def round_trip(self, x, scale_maps=None, out=None):
         return self.synthesis(self.analysis(x, scale_maps), out)
 
+    def round_trip_stream(self, inputs, outputs):
+        """Round trips of a sequence of host maps (pinned tensors of map_shape)
+        into host tensors, double-buffered: the host-to-device copy of map i+1
+        and the device-to-host copy of map i-1 run on their own streams while
+        map i is transformed, so the transfers hide behind the transforms.
+        Same results as ``outputs[i].copy_(round_trip(inputs[i]))``."""
+        th = _device.torch()
+        if len(inputs) != len(outputs):
+            raise ParameterError("inputs and outputs must have the same length")
+        n = len(inputs)
+        if n == 0:
+            return outputs
+        for t in (*inputs, *outputs):
+            if tuple(t.shape) != self.map_shape or t.dtype != self._dtype() or t.is_cuda:
+                raise ParameterError(f"expected host {self._dtype()} tensors of shape {self.map_shape}")
+        dev = f"cuda:{_device.device_index()}"
+        comp = th.cuda.current_stream()
+        h2d, d2h = th.cuda.Stream(), th.cuda.Stream()
+        xin = [th.empty(self.map_shape, dtype=self._dtype(), device=dev) for _ in range(2)]
+        xout = [th.empty(self.map_shape, dtype=self._dtype(), device=dev) for _ in range(2)]
+        scale = self.alloc_scale_maps()
+        in_ready = [th.cuda.Event() for _ in range(2)]
+        in_free = [th.cuda.Event() for _ in range(2)]
+        out_ready = [th.cuda.Event() for _ in range(2)]
+        out_free = [th.cuda.Event() for _ in range(2)]
+        # the buffers are fresh: nothing to wait for before their first use
+        for e in (*in_free, *out_free):
+            e.record(comp)
+        with th.cuda.stream(h2d):
+            h2d.wait_event(in_free[0])
+            xin[0].copy_(inputs[0], non_blocking=True)
+            in_ready[0].record(h2d)
+        for i in range(n):
+            b = i & 1
+            if i + 1 < n:
+                nb = b ^ 1
+                with th.cuda.stream(h2d):
+                    h2d.wait_event(in_free[nb])
+                    xin[nb].copy_(inputs[i + 1], non_blocking=True)
+                    in_ready[nb].record(h2d)
+            comp.wait_event(in_ready[b])
+            comp.wait_event(out_free[b])
+            self.synthesis(self.analysis(xin[b], scale), xout[b])
+            in_free[b].record(comp)
+            out_ready[b].record(comp)
+            with th.cuda.stream(d2h):
+                d2h.wait_event(out_ready[b])
+                outputs[i].copy_(xout[b], non_blocking=True)
+                out_free[b].record(d2h)
+        comp.wait_stream(d2h)
+        comp.wait_stream(h2d)
+        return outputs
+
     def flm(self):
         """View of the plan's f_lm workspace (batch, L*L) complex128."""
         import ctypes

@@ -80,3 +80,25 @@ def test_batch_matches_single(sw):
     recs = sw.wav_synthesis_pixel_batch(decs)
     for m, r in zip(maps, recs):
         assert rel_err(r.values, m.values) <= 1e-10
+
+
+def test_round_trip_stream_matches_round_trip(sw):
+    import torch
+
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
+
+    L = 64
+    cfg = sw.TransformConfig(L, 2.0, 1, scheme=sw.SamplingScheme.MW, multires=True)
+    wt = WaveletTransform(cfg, batch=2, real=False)
+    rng = np.random.default_rng(8)
+    sht = SphericalHarmonicTransform(sw.SamplingScheme.MW, L)
+    ins = []
+    for i in range(5):
+        f = np.stack([sw.gaussian_coeffs(L, rng, real_signal=False).coeffs for _ in range(2)])
+        ins.append(sht.synthesis(torch.from_numpy(f).cuda()).cpu().pin_memory())
+    outs = [torch.empty_like(t).pin_memory() for t in ins]
+    wt.round_trip_stream(ins, outs)
+    torch.cuda.synchronize()
+    for a, b in zip(ins, outs):
+        want = wt.round_trip(a.cuda()).cpu()
+        assert torch.equal(b, want)
