@@ -338,7 +338,7 @@ static int device_tables(int dev, DeviceTables** out) {
 // A set of rings for the Legendre stages: nodes, analysis weights, active
 // ring range per order.  n_north > 0 marks an equator-symmetric set.
 struct RingSet {
-  double *cos_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
+  double *cos_t = nullptr, *omc_t = nullptr, *sin_t = nullptr, *ring_w = nullptr;
   int2* act = nullptr;
   std::vector<int2> act_host;
   int n_north = 0;
@@ -411,6 +411,7 @@ struct GridRes {
     g.n_north = rs.n_north;
     g.n_bins = cplx ? N : k;
     g.cos_t = rs.cos_t;
+    g.omc_t = rs.omc_t;
     g.sin_t = rs.sin_t;
     g.ring_w = rs.ring_w;
     g.act = rs.act;
@@ -458,8 +459,22 @@ static int ring_set(RingSet& rs, const std::vector<double>& theta, const std::ve
       c[t] = -c[tm];
       s[t] = s[tm];
     }
+  // 1 - cos theta with full relative accuracy (2 sin^2(theta/2) in the north,
+  // 1 + |cos theta| in the south): the symmetric kernels step the recursion
+  // with x Q = Q - (1 - x) Q, so polar nodes keep their exact position (a
+  // rounded cos theta moves 1 - x by up to 1e-9 relative at L = 4096).
+  std::vector<double> omc(n);
+  for (int t = 0; t < n; ++t) {
+    if (c[t] >= 0.0) {
+      const ld h = std::sin((ld)theta[t] / 2);
+      omc[t] = (double)(2 * h * h);
+    } else {
+      omc[t] = (double)(1.0L - (ld)c[t]);
+    }
+  }
   rs.n_north = n_north;
   CHECK(upload_new(&rs.cos_t, c));
+  CHECK(upload_new(&rs.omc_t, omc));
   CHECK(upload_new(&rs.sin_t, s));
   CHECK(upload_new(&rs.ring_w, w));
   int* d_mmax = nullptr;

@@ -105,6 +105,7 @@ struct LegGridDev {
   int n_north; // > 0: rings symmetric about the equator (t <-> n_t-1-t), n_north = ceil(n_t/2)
   int n_bins;  // azimuthal bins stored per ring: 2k-1 (complex) or k (real)
   const double* cos_t;
+  const double* omc_t;   // 1 - cos theta to full relative accuracy (symmetric kernels' recursion)
   const double* sin_t;
   const double* ring_w;  // analysis quadrature weight per ring (incl. 2 pi / N factors)
   const int2* act;       // [k] active ring range [lo, hi) per order m
