@@ -183,12 +183,16 @@ static void legendre_pd(int n, ld x, ld& p, ld& dp) {
 
 // Gauss-Legendre nodes ordered north -> south (x descending) with weights,
 // Newton iteration in 80-bit precision (grid.py:93-124 semantics).
-static void gl_nodes(int L, std::vector<double>& theta, std::vector<double>& w) {
+// omc (optional): 1 - x of the 80-bit Newton root, the node the weights belong to.
+static void gl_nodes(int L, std::vector<double>& theta, std::vector<double>& w,
+                     std::vector<long double>* omc = nullptr) {
   theta.resize(L);
   w.resize(L);
+  if (omc) omc->resize(L);
   if (L == 1) {
     theta[0] = std::acos(0.0);
     w[0] = 2.0;
+    if (omc) (*omc)[0] = 1.0L;
     return;
   }
   for (int i = 0; i < L; ++i) {
@@ -206,6 +210,7 @@ static void gl_nodes(int L, std::vector<double>& theta, std::vector<double>& w) 
     ld wi = 2.0L / ((1.0L - x * x) * dp * dp);
     theta[i] = std::acos((double)x);
     w[i] = (double)wi;
+    if (omc) (*omc)[i] = 1.0L - x;
   }
 }
 
@@ -441,8 +446,10 @@ static int upload_new(T** dst, const std::vector<T>& v) {
 
 // Upload a ring set and find its active ring range per order (probe kernel).
 // Symmetric sets (n_north > 0) get exactly mirrored nodes: cos(pi - x) = -cos x.
+// omc_exact (optional): 1 - cos of the exact nodes in long double (else from theta).
 static int ring_set(RingSet& rs, const std::vector<double>& theta, const std::vector<double>& w,
-                    int k, const double* seed_c, int n_north) {
+                    int k, const double* seed_c, int n_north,
+                    const std::vector<long double>* omc_exact = nullptr) {
   const int n = (int)theta.size();
   std::vector<double> c(n), s(n);
   for (int t = 0; t < n; ++t) {
@@ -465,7 +472,9 @@ static int ring_set(RingSet& rs, const std::vector<double>& theta, const std::ve
   // rounded cos theta moves 1 - x by up to 1e-9 relative at L = 4096).
   std::vector<double> omc(n);
   for (int t = 0; t < n; ++t) {
-    if (c[t] >= 0.0) {
+    if (omc_exact) {
+      omc[t] = (double)(*omc_exact)[t];
+    } else if (c[t] >= 0.0) {
       const ld h = std::sin((ld)theta[t] / 2);
       omc[t] = (double)(2 * h * h);
     } else {
@@ -554,15 +563,28 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   g->seed_c = dt->seed_c;
   const int N = g->N, M = 1 << g->logM;
 
+  // exact nodes' 1 - cos theta in long double (recursion in the symmetric kernels)
   std::vector<double> theta, wq;
-  if (scheme == S2W_SCHEME_GL) gl_nodes(k, theta, wq);
-  else mw_nodes(k, theta);
+  std::vector<long double> omc_syn(k), omc_ana(k);
+  if (scheme == S2W_SCHEME_GL) {
+    gl_nodes(k, theta, wq, &omc_syn);
+  } else {
+    mw_nodes(k, theta);
+    for (int t = 0; t < k; ++t) {
+      const ld th = (ld)(2 * t + 1) * PI_L / (ld)(2 * k - 1);
+      omc_syn[t] = th <= PI_L / 2 ? 2 * std::sin(th / 2) * std::sin(th / 2) : 1.0L - std::cos(th);
+    }
+    for (int j = 0; j < k; ++j) {
+      const ld th = (ld)(2 * j + 1) * PI_L / (ld)(2 * k);
+      omc_ana[j] = th <= PI_L / 2 ? 2 * std::sin(th / 2) * std::sin(th / 2) : 1.0L - std::cos(th);
+    }
+  }
   std::vector<double> rw(k);
   for (int t = 0; t < k; ++t) {
     if (scheme == S2W_SCHEME_GL) rw[t] = 2.0 * M_PI * wq[t];
     else rw[t] = (2.0 * M_PI / (double)N) * (t == k - 1 ? 0.5 : 1.0);
   }
-  CHECK(ring_set(g->syn, theta, rw, k, g->seed_c, 0));
+  CHECK(ring_set(g->syn, theta, rw, k, g->seed_c, 0, &omc_syn));
   if (scheme == S2W_SCHEME_GL) {
     g->syn.n_north = (k + 1) / 2;  // GL nodes are symmetric about the equator
     g->ana = g->syn;                // same device tables
@@ -570,7 +592,7 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     // analysis rings of the MW theta stage: theta''_j = (2j+1) pi / 2k, weight pi / k
     std::vector<double> th2(k), w2(k, M_PI / (double)k);
     for (int j = 0; j < k; ++j) th2[j] = (double)((ld)(2 * j + 1) * PI_L / (ld)(2 * k));
-    CHECK(ring_set(g->ana, th2, w2, k, g->seed_c, (k + 1) / 2));
+    CHECK(ring_set(g->ana, th2, w2, k, g->seed_c, (k + 1) / 2, &omc_ana));
   }
 
   // FFT / Bluestein / theta-stage tables
