@@ -136,8 +136,17 @@ def kernel_launches() -> int:
     return int(load().s2w_kernel_launches())
 
 
+_profile_on = False
+
+
 def profile_enable(on: bool) -> None:
+    global _profile_on
     check(load().s2w_profile_enable(int(bool(on))))
+    _profile_on = bool(on)
+
+
+def profile_enabled() -> bool:
+    return _profile_on
 
 
 def profile_read(reset: bool = True) -> dict:

@@ -102,3 +102,27 @@ def test_round_trip_stream_matches_round_trip(sw):
     for a, b in zip(ins, outs):
         want = wt.round_trip(a.cuda()).cpu()
         assert torch.equal(b, want)
+
+
+def test_round_trip_graph_matches_eager(sw):
+    import torch
+
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
+
+    L = 48
+    cfg = sw.TransformConfig(L, 2.0, 0, scheme=sw.SamplingScheme.MW, multires=True)
+    wt = WaveletTransform(cfg, batch=1, real=True)
+    f = sw.gaussian_coeffs(L, np.random.default_rng(12), real_signal=True)
+    sht = SphericalHarmonicTransform(sw.SamplingScheme.MW, L)
+    x = sht.synthesis(torch.from_numpy(f.coeffs[None].copy()).cuda(), real=True)
+    scale = wt.alloc_scale_maps()
+    out = torch.empty_like(x)
+    want = wt.round_trip(x, wt.alloc_scale_maps(), torch.empty_like(x)).clone()
+    for _ in range(3):
+        wt.round_trip_graph(x, scale, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+    x.mul_(2.0)  # replays read the buffers' current contents
+    wt.round_trip_graph(x, scale, out)
+    torch.cuda.synchronize()
+    assert torch.allclose(out, 2.0 * want, rtol=1e-12, atol=1e-12)
