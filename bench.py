@@ -41,6 +41,23 @@ CONFIGS = {
 }
 
 
+def _traffic(cfgname, kernel, mode):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu capture
+    (profiles/roofline_traffic.json), or None when none matches this workload."""
+    import json
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "roofline_traffic.json")
+    if mode == "shard" or not os.path.exists(path):
+        return None
+    try:
+        with open(path) as fh:
+            rec = json.load(fh).get(cfgname, {}).get(kernel)
+        return int(rec["dram_bytes_per_launch"]) if rec else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def spectrum(name, L):
     ell = np.arange(L, dtype=np.float64)
     if name == "flat":
@@ -328,7 +345,8 @@ def run_ours(args, cfgname):
             "bound": "fp64", "kernel": dom,
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if achieved else None,
-            "traffic": None,
+            "traffic": _traffic(cfgname, dom, mode),
+            "traffic_unit": "bytes per launch (DRAM read + write, ncu --set full)",
             "flops_per_launch": fl[dom] * shard_frac,
             "peak_source": f"measured in this run: DFMA {fp64_peak:.1f}, DMMA {dmma_peak:.1f} "
                            "TFLOP/s (s2w_fp64_peak / s2w_dmma_peak); MEASURED_PEAKS.json has "
