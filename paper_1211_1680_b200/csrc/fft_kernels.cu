@@ -17,8 +17,10 @@
 // All odd-length DFTs (N = 2L-1) are Bluestein chirp-z transforms over the
 // power-of-two shared-memory FFT in fft.cuh.
 #include <algorithm>
+#include <stdlib.h>
 
 #include "fft.cuh"
+#include "pfa.cuh"
 #include "s2w_internal.h"
 
 namespace s2w {
@@ -171,6 +173,91 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_inv_kernel(PhiInvArgs a)
   }
 }
 
+// ---------------------------------------------------------------- phi at N = 4095
+// Ring DFTs of length 4095 (L = 2048) by the prime-factor engine (pfa.cuh):
+// one ring (or one real ring pair) per CTA, 64 KiB of shared memory, same
+// outputs and layouts as phi_fwd_kernel / phi_inv_kernel.
+constexpr int PFA_T = 128;
+
+__global__ void __launch_bounds__(PFA_T) phi_fwd_pfa_kernel(PhiFwdArgs a) {
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  const int N = PFA_N, tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const long long base_a = ((long long)set * a.n_rings + ta) * N;
+  for (int n = tid; n < N; n += PFA_T) {
+    double2 x;
+    if (!a.real) x = __ldg(reinterpret_cast<const double2*>(a.in) + base_a + n);
+    else x = make_double2(__ldg(&a.in[base_a + n]), vb ? __ldg(&a.in[base_a + N + n]) : 0.0);
+    buf[n] = x;
+  }
+  __syncthreads();
+  pfa4095<false>(buf, tid, PFA_T);
+  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
+  for (int mi = tid; mi < a.n_bins; mi += PFA_T) {
+    const double2 z = buf[pfa_pos(mi)];
+    if (!a.real) {
+      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+    } else {
+      const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
+      const double h = 0.5 * a.scale;
+      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
+      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PFA_T) phi_inv_pfa_kernel(PhiInvArgs a) {
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  const int N = PFA_N, tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * a.n_bins;
+  const double2* Gb = Ga + a.n_bins;
+  for (int n = tid; n < N; n += PFA_T) {
+    double2 x;
+    if (!a.real) {
+      x = __ldg(&Ga[n]);
+    } else {
+      double2 X, Y = make_double2(0.0, 0.0);
+      if (n < a.n_bins) {
+        X = __ldg(&Ga[n]);
+        if (vb) Y = __ldg(&Gb[n]);
+        if (n == 0) X.y = Y.y = 0.0;
+      } else {
+        X = cconj(__ldg(&Ga[N - n]));
+        if (vb) Y = cconj(__ldg(&Gb[N - n]));
+      }
+      x = cadd(X, cmul_pi(Y));
+    }
+    buf[n] = x;
+  }
+  __syncthreads();
+  pfa4095<true>(buf, tid, PFA_T);
+  const int pole_ring = (N + 1) / 2 - 1 - a.t_offset;
+  const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
+  const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
+  const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
+  const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+  for (int q = tid; q < N; q += PFA_T) {
+    const double2 v = buf[pfa_pos(q)];
+    if (a.real) {
+      a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
+      if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
+    } else {
+      reinterpret_cast<double2*>(a.out)[ob + q] = hard_thresh(pa ? pva : v, a.thresh);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- MW theta stage
 // Parity pairing: the operator (extension -> band-limited |sin| product ->
 // first k rings) commutes with the reflection R: n -> N-1-n.  An even-m row
@@ -222,7 +309,9 @@ S2W_DEV void theta_store(const ThetaPair& P, const ThetaArgs& a, int t, double2 
   if (P.ho) P.ho[t] = cadd(cscale(csub(wt, wr), 0.5), dr);
 }
 
-template <int LOGM>
+// PFA: N = 4095, the DFT_N of step 2 runs on the prime-factor engine
+// (natural order in the first 4095 slots, no chirps).
+template <int LOGM, bool PFA = false>
 __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
@@ -244,15 +333,34 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
       const int n = n0 + u * GS;
       const bool in = valid && n < N;
       x[u] = in ? theta_ext(P, n, k) : make_double2(0.0, 0.0);
-      c[u] = in ? __ldg(&T.chirp[n]) : make_double2(0.0, 0.0);
+      c[u] = in ? (PFA ? make_double2(1.0, 0.0) : __ldg(&T.chirp[n])) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int n = n0 + u * GS;
-      if (n < M) buf[swz(n)] = cmul(x[u], c[u]);
+      if (n < M) buf[PFA ? n : swz(n)] = cmul(x[u], c[u]);
     }
   }
   __syncthreads();
+  if constexpr (PFA) {
+    // 2-3. DFT_N by the prime-factor engine; a_{m'} = X_bin e^{-i pi m'/N} / N
+    //      (= ph1 conj(c_bin)), moved to the swizzled length-M circle
+    static_assert(!PFA || 8 * GS >= PFA_N, "one pass of register moves");
+    pfa4095<false>(buf, gtid, GS);
+    double2 av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = gtid + u * GS;
+      av[u] = (bin < N) ? cmulc(cmul(buf[pfa_pos(bin)], __ldg(&T.ph1[bin])), __ldg(&T.chirp[bin]))
+                        : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bin = gtid + u * GS;
+      if (bin < N) buf[swz(bin < k ? bin : M - N + bin)] = av[u];
+    }
+  } else {
   // 2. DFT_N (Bluestein)
   fft_conv<LOGM, GS>(buf, tw, T.bl_fwd, gtid);
   // 3. Fourier coefficients a_{m'} = c_bin e^{-i pi m'/N} conv[bin] / N, laid out
@@ -271,6 +379,7 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
       const double2 v = cmul(buf[swz(bin)], ph[u]);
       buf[swz(bin < k ? bin : M - N + bin)] = v;
     }
+  }
   }
   __syncthreads();
   for (int n = k + gtid; n < M - k + 1; n += GS) buf[swz(n)] = make_double2(0.0, 0.0);
@@ -371,7 +480,8 @@ S2W_DEV void theta_syn_store(const ThetaSynRow& R, const ThetaSynArgs& a, int t,
   if (R.co >= 0) R.out[(size_t)t * a.n_bins + R.co] = cscale(csub(wt, wr), 0.5);
 }
 
-template <int LOGM>
+// PFA: N = 4095, the inverse DFT_N of step 4 runs on the prime-factor engine.
+template <int LOGM, bool PFA = false>
 __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
@@ -422,6 +532,21 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArg
     }
   }
   __syncthreads();
+  if constexpr (PFA) {
+    // 4. inverse DFT_N by the prime-factor engine (input without the Bluestein
+    //    chirp conj(c_n) folded into ph4: times c_n); rings t and N-1-t
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = gtid + u * GS;
+      if (n < N) buf[n] = cmul(xv[u], __ldg(&T.chirp[n]));
+    }
+    __syncthreads();
+    pfa4095<true>(buf, gtid, GS);
+    if (!valid) return;
+    for (int t = gtid; t < k; t += GS)
+      theta_syn_store(R, a, t, buf[pfa_pos(t)], buf[pfa_pos(N - 1 - t)]);
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int n = gtid + u * GS;
@@ -836,15 +961,32 @@ int fft_tw_elems(int logE) { return fft_ntw(logE); }
     default: return cudaErrorInvalidValue;                                   \
   }
 
+template <class Args>
+static cudaError_t pfa_launch(void (*kern)(Args), Args a, int n_rows, cudaStream_t st) {
+  const size_t smem = 4096 * sizeof(double2);
+  cudaError_t e = set_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<n_rows, PFA_T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// the prime-factor engine serves N = 4095 (L = 2048) unless S2W_NO_PFA is set
+static bool use_pfa(int N) {
+  static const bool off = getenv("S2W_NO_PFA") != nullptr;
+  return N == PFA_N && !off;
+}
+
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N)) return pfa_launch(phi_fwd_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_fwd_kernel, phi_fwd_split_kernel, a, n_rows, st)
 }
 
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N)) return pfa_launch(phi_inv_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_inv_kernel, phi_inv_split_kernel, a, n_rows, st)
 }
 
@@ -865,12 +1007,15 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
 cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && a.T.logM == 13)
+    return row_launch(theta_syn_kernel<13, true>, 13, a, n_rows, st);
   S2W_FFT_DISPATCH(theta_syn_kernel, theta_syn_split_kernel, a, n_rows, st)
 }
 
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && a.T.logM == 13) return row_launch(theta_kernel<13, true>, 13, a, n_rows, st);
   S2W_FFT_DISPATCH(theta_kernel, theta_split_kernel, a, n_rows, st)
 }
 

@@ -188,3 +188,18 @@ def test_split_fft_sizes_round_trip(sw, scheme, real, L):
     x = sht.synthesis(torch.from_numpy(f[None].copy()).cuda(), real=real)
     back = sht.analysis(x).cpu().numpy()[0]
     assert np.abs(back - f).max() <= 2e-10 * max(1.0, np.abs(f).max())
+
+
+@pytest.mark.parametrize("scheme", ["GL", "MW"])
+@pytest.mark.parametrize("real", [True, False])
+def test_round_trip_L2048_pfa(sw, scheme, real):
+    """L = 2048 (N = 4095): ring DFTs and MW theta stages on the prime-factor engine."""
+    import torch
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform
+
+    L = 2048
+    f = sw.gaussian_coeffs(L, np.random.default_rng(5 + real), real_signal=real).coeffs
+    sht = SphericalHarmonicTransform(getattr(sw.SamplingScheme, scheme), L)
+    x = sht.synthesis(torch.from_numpy(f[None].copy()).cuda(), real=real)
+    back = sht.analysis(x).cpu().numpy()[0]
+    assert np.abs(back - f).max() <= 1e-10 * max(1.0, np.abs(f).max())

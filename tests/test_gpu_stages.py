@@ -99,3 +99,18 @@ def test_phi_stages_split_mode_vs_numpy(env, L, real):
     F = (np.fft.rfft(want, axis=-1) if real else np.fft.fft(want, axis=-1)) / N
     got_f = _run_forward(env, 0, L, want if not real else want.astype(complex), real, 0)
     assert np.abs(got_f - np.swapaxes(F, 1, 2)).max() <= 1e-14 * np.abs(F).max() * np.log2(N)
+
+
+@pytest.mark.parametrize("real", [True, False])
+def test_theta_stage_pfa_L2048_vs_oracle(env, real):
+    """L = 2048: the theta stage's DFT_4095 runs on the prime-factor engine."""
+    from oracle import oracle as orc
+
+    L = 2048
+    rng = np.random.default_rng(11 + real)
+    maps = rng.standard_normal((1, L, 2 * L - 1))
+    if not real:
+        maps = maps + 1j * rng.standard_normal((1, L, 2 * L - 1))
+    H = _run_forward(env, 1, L, maps if not real else maps.astype(complex), real, 1)
+    Href = orc.mw_theta_stage_rings(orc.rings_forward(maps, L, real), L, real)
+    assert np.abs(H - Href).max() <= 1e-12 * np.abs(Href).max()
