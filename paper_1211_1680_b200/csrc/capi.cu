@@ -356,7 +356,9 @@ struct GridRes {
   RingSet syn, ana;
   double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr,
-          *bl_fwd2 = nullptr, *ph4 = nullptr, *ph2d = nullptr, *ph4d = nullptr;
+          *bl_fwd2 = nullptr, *ph4 = nullptr, *ph2d = nullptr, *ph4d = nullptr, *tw12 = nullptr,
+          *phA = nullptr, *phS = nullptr;
+  double* w2s = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
   int2 *pairs_r = nullptr, *pairs_c = nullptr;
@@ -393,6 +395,10 @@ struct GridRes {
     t.ph4 = ph4;
     t.ph2d = ph2d;
     t.ph4d = ph4d;
+    t.tw12 = tw12;
+    t.w2s = w2s;
+    t.phA = phA;
+    t.phS = phS;
     return t;
   }
   // MW synthesis runs on the (symmetric) analysis rings and is resampled to
@@ -679,6 +685,29 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
   CHECK(upload_new(&g->ph4, ph4));
   CHECK(upload_new(&g->ph2d, ph2d));
   CHECK(upload_new(&g->ph4d, ph4d));
+  if (N == 4095) {
+    // k2 stage kernels (fft_kernels.cu): 4096-point engine twiddles, the |sin|
+    // series on one parity class w_hat(2d) = 4/(1 - 4d^2), |d| <= 2047, and the
+    // bin phases of the theta / theta_syn stages with the chirps folded out
+    const int M2 = 4096;
+    std::vector<cld> w2(M2, cld(0, 0));
+    for (int d = -(M2 / 2 - 1); d <= M2 / 2 - 1; ++d)
+      w2[(d + M2) % M2] = cld(4.0L / (1.0L - 4.0L * (ld)d * (ld)d), 0);
+    std::vector<double2> phA(N), phS(N);
+    for (int n = 0; n < N; ++n) {
+      const int q = n < k ? n : n - N;
+      const ld a1 = -PI_L * (ld)q / (ld)N;
+      phA[n] = d2(cld(std::cos(a1), std::sin(a1)) / (ld)N);
+      const ld a2 = -PI_L * (ld)q / (ld)N2 + PI_L * (ld)q / (ld)N;
+      phS[n] = d2(cld(std::cos(a2), std::sin(a2)) / (ld)N2);
+    }
+    CHECK(upload_new(&g->tw12, pass_twiddles(12)));
+    std::vector<double> w2r;
+    for (const double2& z : spectrum_brev(w2)) w2r.push_back(z.x);  // Im ~ 1e-19: exact zero
+    CHECK(upload_new(&g->w2s, w2r));
+    CHECK(upload_new(&g->phA, phA));
+    CHECK(upload_new(&g->phS, phS));
+  }
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   g_grids[key] = g;
   *out = g;

@@ -144,17 +144,26 @@ S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, i
     double2 v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = buf[sb ^ swz(k << LS)];
-    double2 w[16];
-    powers16(w, tw[j * TWS]);
-    if constexpr (!INV) {
-      dif<4>(v);
+    // twiddle powers u^1..u^7 and u^8; u^(8+k) = u^8 u^k formed at use (the
+    // same products as powers16, with half of them live at a time)
+    double2 w[8];
+    const double2 u = tw[j * TWS];
+    w[1] = u;
+    w[2] = cmul(u, u);
+    w[3] = cmul(w[2], u);
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], u);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
+    const double2 w8 = cmul(w[4], w[4]);
+    if constexpr (!INV) dif<4>(v);
 #pragma unroll
-      for (int i = 1; i < 16; ++i) v[i] = cmul(v[i], w[brev4(i)]);
-    } else {
-#pragma unroll
-      for (int i = 1; i < 16; ++i) v[i] = cmulc(v[i], w[brev4(i)]);
-      adj<4>(v);
+    for (int kk = 1; kk < 16; ++kk) {
+      const double2 wk = kk < 8 ? w[kk] : (kk == 8 ? w8 : cmul(w8, w[kk - 8]));
+      const int i = brev4(kk);
+      v[i] = INV ? cmulc(v[i], wk) : cmul(v[i], wk);
     }
+    if constexpr (INV) adj<4>(v);
 #pragma unroll
     for (int k = 0; k < 16; ++k) buf[sb ^ swz(k << LS)] = v[k];
   }
@@ -172,14 +181,39 @@ S2W_DEV void conv_core(double2* __restrict__ buf, const double2* __restrict__ ta
     const int b = gtid + it * GS;
     if (NB % GS != 0 && b >= NB) break;
     const int sb = swz(b * R);
-    double2 v[R], t[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
+    double2 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];
     dif<CB>(v);
 #pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], t[i]);
+    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], __ldg(&tab[b * R + i]));
+    adj<CB>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[sb ^ swz(i)] = v[i];
+  }
+}
+
+// conv_core with a real spectrum (a real, even convolution kernel): half the
+// table bytes and registers.
+template <int LOGM, int GS>
+S2W_DEV void conv_core_real(double2* __restrict__ buf, const double* __restrict__ tab, int gtid) {
+  constexpr int CB = LOGM - 4 * fft_k16(LOGM);
+  constexpr int R = 1 << CB;
+  constexpr int NB = (1 << LOGM) / R;
+#pragma unroll
+  for (int it = 0; it < (NB + GS - 1) / GS; ++it) {
+    const int b = gtid + it * GS;
+    if (NB % GS != 0 && b >= NB) break;
+    const int sb = swz(b * R);
+    double t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
+    double2 v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];
+    dif<CB>(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = cscale(v[i], t[i]);
     adj<CB>(v);
 #pragma unroll
     for (int i = 0; i < R; ++i) buf[sb ^ swz(i)] = v[i];
@@ -247,6 +281,15 @@ S2W_DEV void fft_conv(double2* buf, const double2* tw, const double2* __restrict
                       int gtid) {
   fwd_passes<LOGM, GS, 0>(buf, tw, gtid);
   conv_core<LOGM, GS>(buf, tab, gtid);
+  __syncthreads();
+  inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
+}
+
+// fft_conv with a real spectrum table (conv_core_real).
+template <int LOGM, int GS>
+S2W_DEV void fft_conv_real(double2* buf, const double2* tw, const double* __restrict__ tab, int gtid) {
+  fwd_passes<LOGM, GS, 0>(buf, tw, gtid);
+  conv_core_real<LOGM, GS>(buf, tab, gtid);
   __syncthreads();
   inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
 }

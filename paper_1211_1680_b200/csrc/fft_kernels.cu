@@ -869,6 +869,322 @@ __global__ void __launch_bounds__(SPLIT_T) theta_syn_split_kernel(ThetaSynArgs a
   }
 }
 
+// =====================================================================
+// k2: the N = 4095 (L = 2048) stages, one row (ring, or theta column pair)
+// per CTA.  The row arrives by one bulk copy (TMA, cp.async.bulk) completed on
+// an mbarrier -- no per-thread load loop -- and every buffer is sized for the
+// prime-factor engine (4096 slots = 64 KiB), so two or three CTAs share an SM
+// and one CTA's copies overlap another's shared-memory passes.
+//  * phi_fwd_k2 / phi_inv_k2: ring DFTs (same I/O as phi_fwd/inv_kernel).
+//  * theta_syn_k2: direct 4096-point FFT + prime-factor inverse DFT_4095.
+//  * theta_k2: the |sin| convolution on the parity classes of the Fourier
+//    index: w_hat(p) vanishes at odd p, so H'(q) = sum_m' a_m' w_hat(q - m')
+//    couples only q and m' of equal parity.  Each class is a linear
+//    convolution of <= 2048 coefficients whose outputs are needed at <= 2048
+//    points, with kernel differences |q - m'|/2 <= 2047: two exact 4096-point
+//    cyclic convolutions (kernel w_hat(2d)) replace the 8192-point one and the
+//    row fits 96 KiB (two CTAs per SM).
+// =====================================================================
+constexpr int K2_N = 4095, K2_M = 4096, K2_K = 2048;
+constexpr int K2_NTW = 272;  // fft_ntw(12)
+static_assert(K2_NTW == fft_ntw(12), "4096-point pass twiddles");
+#ifndef S2W_K2_T
+#define S2W_K2_T 256
+#endif
+constexpr int K2_T = S2W_K2_T;
+
+template <int T>
+__global__ void __launch_bounds__(T) phi_fwd_k2_kernel(PhiFwdArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;
+  uint64_t* mb = reinterpret_cast<uint64_t*>(smem + K2_M);
+  constexpr int N = K2_N, U = (K2_N + T - 1) / T;
+  const int tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const long long base_a = ((long long)set * a.n_rings + ta) * N;
+  // rows are contiguous: a complex ring, or a real ring pair (launcher checks alignment)
+  const unsigned bytes = a.real ? (vb ? 2u : 1u) * N * 8u : N * 16u;
+  if (tid == 0) {
+    mbar_init(mb, 1);
+    mbar_expect_tx(mb, bytes);
+    bulk_g2s(buf, a.in + (a.real ? base_a : 2 * base_a), bytes, mb);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  if (a.real) {
+    // [ring a | ring b] doubles -> interleaved z = a + i b
+    const double* r = reinterpret_cast<const double*>(buf);
+    double xr[U], xi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      xr[u] = n < N ? r[n] : 0.0;
+      xi[u] = (n < N && vb) ? r[N + n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      if (n < N) buf[n] = make_double2(xr[u], xi[u]);
+    }
+    __syncthreads();
+  }
+  pfa4095<false>(buf, tid, T);
+  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
+  for (int mi = tid; mi < a.n_bins; mi += T) {
+    const double2 z = buf[pfa_pos(mi)];
+    if (!a.real) {
+      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+    } else {
+      const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
+      const double h = 0.5 * a.scale;
+      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
+      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) phi_inv_k2_kernel(PhiInvArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;
+  uint64_t* mb = reinterpret_cast<uint64_t*>(smem + K2_M);
+  constexpr int N = K2_N, U = (K2_N + T - 1) / T;
+  const int tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const int nb = a.n_bins;
+  const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * nb;
+  const double2* Gb = Ga + nb;
+  const unsigned bytes = (vb ? 2u : 1u) * nb * 16u;
+  if (tid == 0) {
+    mbar_init(mb, 1);
+    mbar_expect_tx(mb, bytes);
+    bulk_g2s(buf, Ga, bytes, mb);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  if (a.real) {
+    // Hermitian spectra of the two rings (irfft ignores Im of the DC bin)
+    double2 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      x[u] = make_double2(0.0, 0.0);
+      if (n < N) {
+        const bool lo = n < nb;
+        const int src = lo ? n : N - n;
+        double2 X = buf[src], Y = vb ? buf[nb + src] : make_double2(0.0, 0.0);
+        if (!lo) {
+          X = cconj(X);
+          Y = cconj(Y);
+        }
+        if (n == 0) X.y = Y.y = 0.0;
+        x[u] = cadd(X, cmul_pi(Y));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      if (n < N) buf[n] = x[u];
+    }
+    __syncthreads();
+  }
+  pfa4095<true>(buf, tid, T);
+  const int pole_ring = (N + 1) / 2 - 1 - a.t_offset;
+  const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
+  const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
+  const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
+  const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+  for (int q = tid; q < N; q += T) {
+    const double2 v = buf[pfa_pos(q)];
+    if (a.real) {
+      a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
+      if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
+    } else {
+      reinterpret_cast<double2*>(a.out)[ob + q] = hard_thresh(pa ? pva : v, a.thresh);
+    }
+  }
+}
+
+// Arm the barrier and issue the bulk copies of the 4096-point pass twiddles
+// and a theta column pair (ge -> dst[0, k), go -> dst[k, 2k)).
+S2W_DEV void k2_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* dst, const double2* ge,
+                      const double2* go) {
+  constexpr unsigned col = K2_K * 16u;
+  mbar_init(mb, 1);
+  mbar_expect_tx(mb, K2_NTW * 16u + (ge ? col : 0u) + (go ? col : 0u));
+  bulk_g2s(tw, gtw, K2_NTW * 16u, mb);
+  if (ge) bulk_g2s(dst, ge, col, mb);
+  if (go) bulk_g2s(dst + K2_K, go, col, mb);
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 2) theta_syn_k2_kernel(ThetaSynArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;           // [4096]
+  double2* tw = smem + K2_M;     // [272]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(tw + K2_NTW);
+  constexpr int N = K2_N, k = K2_K, U = K2_M / T;
+  const FftTablesDev& F = a.T;
+  const int tid = threadIdx.x;
+  const ThetaSynRow R = theta_syn_row(a, blockIdx.x, true);
+  if (tid == 0) k2_issue(mb, tw, F.tw12, buf, R.ge, R.go);
+  __syncthreads();
+  mbar_wait(mb, 0);
+  // 1. parity extension on the 2k analysis points
+  double2 x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 1 - n;
+    const double2 e = R.ge ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = R.go ? buf[k + src] : make_double2(0.0, 0.0);
+    x[u] = lo ? cadd(e, o) : csub(e, o);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  __syncthreads();
+  // 2. DFT_4096 (direct)
+  fft_fwd<12, T, 0>(buf, tw, tid);
+  // 3. DFT_N input (bit-reversed source slot, n >= k reads bin n + 1)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    x[u] = make_double2(0.0, 0.0);
+    if (n < N) {
+      const int src = n < k ? n : n + 1;
+      x[u] = cmul(buf[swz(fft_brev<12>(src))], __ldg(&F.phS[n]));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    if (n < N) buf[n] = x[u];
+  }
+  __syncthreads();
+  // 4. inverse DFT_N by the prime-factor engine; rings t and N-1-t
+  pfa4095<true>(buf, tid, T);
+  for (int t = tid; t < k; t += T) theta_syn_store(R, a, t, buf[pfa_pos(t)], buf[pfa_pos(N - 1 - t)]);
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 2) theta_k2_kernel(ThetaArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;               // [4096]
+  double2* side = smem + K2_M;       // [2048]
+  double2* tw = side + K2_K;         // [272]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(tw + K2_NTW);
+  constexpr int N = K2_N, k = K2_K, U = K2_M / T, V = K2_K / T;
+  const FftTablesDev& F = a.T;
+  const int tid = threadIdx.x;
+  bool has_e, has_o;
+  {
+    // (the pair is re-read for the stores: nothing stays live across the FFTs)
+    const ThetaPair P = theta_pair(a, blockIdx.x, true);
+    has_e = P.ge != nullptr;
+    has_o = P.go != nullptr;
+    if (tid == 0) k2_issue(mb, tw, F.tw12, buf, P.ge, P.go);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  // 1. parity extension to the full circle (natural order for the PFA)
+  double2 x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 2 - n;
+    const double2 e = (has_e && n < N) ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = (has_o && n < N) ? buf[k + src] : make_double2(0.0, 0.0);
+    x[u] = lo ? cadd(e, o) : csub(e, o);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    if (n < N) buf[n] = x[u];
+  }
+  __syncthreads();
+  // 2. DFT_N
+  pfa4095<false>(buf, tid, T);
+  // 3. Fourier coefficients a_q = X_bin e^{-i pi q/N} / N by parity of q:
+  //    even q = 2b -> buf slot b (mod 4096), odd q = 2b+1 -> side slot b (mod 2048)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    x[u] = bin < N ? cmul(buf[pfa_pos(bin)], __ldg(&F.phA[bin])) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    if (bin >= N) continue;
+    const int q = bin < k ? bin : bin - N;
+    if (q & 1) side[((q - 1) >> 1) & (K2_K - 1)] = x[u];
+    else buf[swz((q >> 1) & (K2_M - 1))] = x[u];
+  }
+  for (int s = 1024 + tid; s <= 3072; s += T) buf[swz(s)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
+  //      a); in between, even outputs -> side, odd coefficients -> buf
+#pragma unroll 1
+  for (int cls = 0; cls < 2; ++cls) {
+    fft_conv_real<12, T>(buf, tw, F.w2s, tid);
+    if (cls) break;
+    double2 ev[V], od[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 1024 ? i : i - 2048;
+      ev[u] = buf[swz(aa & (K2_M - 1))];
+      od[u] = side[aa & (K2_K - 1)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 1024 ? i : i - 2048;
+      buf[swz(aa & (K2_M - 1))] = od[u];
+      side[aa & (K2_K - 1)] = ev[u];
+      buf[swz(1024 + i)] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+  // 7. evaluation on the analysis rings: X'_n = conj(H'(q)) e^{-i pi q/N2}, n = q mod N2
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const int q = n < k ? n : n - K2_M;
+    double2 h = make_double2(0.0, 0.0);
+    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (K2_M - 1))] : side[(q >> 1) & (K2_K - 1)];
+    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  __syncthreads();
+  // 8. direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
+  fft_fwd<12, T, 0>(buf, tw, tid);
+  const ThetaPair P = theta_pair(a, blockIdx.x, true);
+  for (int t = tid; t < k; t += T) {
+    const double2 wt = cconj(buf[swz(fft_brev<12>(t))]);
+    const double2 wr = cconj(buf[swz(fft_brev<12>(K2_M - 1 - t))]);
+    theta_store(P, a, t, wt, wr);
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static cudaError_t set_smem(const void* fn, size_t smem) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -976,9 +1292,29 @@ static bool use_pfa(int N) {
   return N == PFA_N && !off;
 }
 
+// k2 kernels: 64 KiB row buffer + barrier (+ side buffer and twiddles for theta)
+static size_t k2_smem(int side, bool tw) {
+  return ((size_t)K2_M + side + (tw ? K2_NTW : 0)) * sizeof(double2) + 16;
+}
+template <class Args>
+static cudaError_t k2_launch(void (*kern)(Args), Args a, int n_rows, size_t smem, cudaStream_t st) {
+  cudaError_t e = set_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<n_rows, K2_T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+// bulk copies need 16-byte aligned rows: complex buffers always are (if the
+// base is); real ring pairs need an even ring count
+static bool k2_ok(const void* base, bool real_pairs, int n_rings) {
+  static const bool off = getenv("S2W_NO_K2") != nullptr;
+  return !off && ((uintptr_t)base & 15) == 0 && (!real_pairs || (n_rings % 2) == 0);
+}
+
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && k2_ok(a.in, a.real, a.n_rings))
+    return k2_launch(phi_fwd_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
   if (use_pfa(a.T.N)) return pfa_launch(phi_fwd_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_fwd_kernel, phi_fwd_split_kernel, a, n_rows, st)
 }
@@ -986,6 +1322,8 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && k2_ok(a.in, false, a.n_rings) && a.n_bins <= (a.real ? K2_K : K2_N))
+    return k2_launch(phi_inv_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
   if (use_pfa(a.T.N)) return pfa_launch(phi_inv_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_inv_kernel, phi_inv_split_kernel, a, n_rows, st)
 }
@@ -1007,6 +1345,8 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
 cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && a.T.tw12 && k2_ok(a.in, false, 0))
+    return k2_launch(theta_syn_k2_kernel<K2_T>, a, n_rows, k2_smem(0, true), st);
   if (use_pfa(a.T.N) && a.T.logM == 13)
     return row_launch(theta_syn_kernel<13, true>, 13, a, n_rows, st);
   S2W_FFT_DISPATCH(theta_syn_kernel, theta_syn_split_kernel, a, n_rows, st)
@@ -1015,6 +1355,8 @@ cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_pfa(a.T.N) && a.T.tw12 && k2_ok(a.in, false, 0))
+    return k2_launch(theta_k2_kernel<K2_T>, a, n_rows, k2_smem(K2_K, true), st);
   if (use_pfa(a.T.N) && a.T.logM == 13) return row_launch(theta_kernel<13, true>, 13, a, n_rows, st);
   S2W_FFT_DISPATCH(theta_kernel, theta_split_kernel, a, n_rows, st)
 }

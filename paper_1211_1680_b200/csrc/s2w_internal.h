@@ -34,6 +34,12 @@ struct FftTablesDev {
   // N2 = M/2 (k a power of two; the DFT_N2 steps are direct half-size FFTs):
   const double2* ph2d;    // [N2] exp(-i pi q(n)/N2)  (conjugated evaluation input)
   const double2* ph4d;    // [N]  e^{-i pi q/N2} e^{i pi q/N} conj(c_n) / N2
+  // N = 4095 (k = 2048) stage kernels (fft_kernels.cu, "k2"):
+  const double2* tw12;    // radix-16 pass twiddles of the 4096-point engine
+  const double* w2s;      // [4096] FFT(w_hat(2d), circular)/4096 (real: the kernel is real and even),
+                          //        the |sin| series on one parity class, bit-reversed
+  const double2* phA;     // [N]  e^{-i pi q/N} / N  (theta: DFT_N bin -> Fourier coefficient)
+  const double2* phS;     // [N]  e^{-i pi q/N2} e^{i pi q/N} / N2  (theta_syn: DFT_N2 bin -> DFT_N input)
 };
 
 struct PhiFwdArgs {
