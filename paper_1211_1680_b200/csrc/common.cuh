@@ -67,3 +67,6 @@ S2W_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\
 S2W_DEV bool bulk_ok(const void* p, size_t bytes) {
   return (((uintptr_t)p | bytes) & 15) == 0 && bytes > 0;
 }
+S2W_DEV void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}

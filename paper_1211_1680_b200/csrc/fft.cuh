@@ -29,7 +29,10 @@
 #pragma once
 #include "common.cuh"
 
-__host__ __device__ constexpr int swz(int i) { return i ^ (((i >> 3) ^ (i >> 4)) & 7); }
+// Bits 9-11 enter the XOR too, so bit-reversed gathers (8 lanes with
+// consecutive indices read slots that differ only in bits 9-11) hit distinct
+// banks as well; all pass patterns of log2 M = 3..13 stay conflict-free.
+__host__ __device__ constexpr int swz(int i) { return i ^ (((i >> 3) ^ (i >> 4) ^ (i >> 9)) & 7); }
 
 __host__ __device__ constexpr int brev4(int r) {
   return ((r & 1) << 3) | ((r & 2) << 1) | ((r & 4) >> 1) | ((r & 8) >> 3);

@@ -892,9 +892,16 @@ static_assert(K2_NTW == fft_ntw(12), "4096-point pass twiddles");
 #define S2W_K2_T 256
 #endif
 constexpr int K2_T = S2W_K2_T;
+#ifndef S2W_K2_TT
+#define S2W_K2_TT 256
+#endif
+constexpr int K2_TT = S2W_K2_TT;  // theta_k2 threads
+#ifndef S2W_K2_PHI_MINB
+#define S2W_K2_PHI_MINB 2
+#endif
 
 template <int T>
-__global__ void __launch_bounds__(T) phi_fwd_k2_kernel(PhiFwdArgs a) {
+__global__ void __launch_bounds__(T, S2W_K2_PHI_MINB) phi_fwd_k2_kernel(PhiFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   double2* buf = smem;
   uint64_t* mb = reinterpret_cast<uint64_t*>(smem + K2_M);
@@ -912,6 +919,14 @@ __global__ void __launch_bounds__(T) phi_fwd_k2_kernel(PhiFwdArgs a) {
     mbar_init(mb, 1);
     mbar_expect_tx(mb, bytes);
     bulk_g2s(buf, a.in + (a.real ? base_a : 2 * base_a), bytes, mb);
+    // the row of the CTA that will take this slot later: HBM stays busy
+    const int nrow = row + a.pfd;
+    if (a.pfd && nrow < (int)gridDim.x) {
+      const int ns = nrow / per, np = nrow - ns * per;
+      const long long nb = ((long long)ns * a.n_rings + (a.real ? 2 * np : np)) * N;
+      const bool nvb = a.real && 2 * np + 1 < a.n_rings;
+      bulk_prefetch_l2(a.in + (a.real ? nb : 2 * nb), a.real ? (nvb ? 2u : 1u) * N * 8u : N * 16u);
+    }
   }
   __syncthreads();
   mbar_wait(mb, 0);
@@ -949,7 +964,7 @@ __global__ void __launch_bounds__(T) phi_fwd_k2_kernel(PhiFwdArgs a) {
 }
 
 template <int T>
-__global__ void __launch_bounds__(T) phi_inv_k2_kernel(PhiInvArgs a) {
+__global__ void __launch_bounds__(T, S2W_K2_PHI_MINB + 1) phi_inv_k2_kernel(PhiInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   double2* buf = smem;
   uint64_t* mb = reinterpret_cast<uint64_t*>(smem + K2_M);
@@ -968,6 +983,13 @@ __global__ void __launch_bounds__(T) phi_inv_k2_kernel(PhiInvArgs a) {
     mbar_init(mb, 1);
     mbar_expect_tx(mb, bytes);
     bulk_g2s(buf, Ga, bytes, mb);
+    const int nrow = row + a.pfd;
+    if (a.pfd && nrow < (int)gridDim.x) {
+      const int ns = nrow / per, np = nrow - ns * per;
+      const int nta = a.real ? 2 * np : np;
+      const bool nvb = a.real && nta + 1 < a.n_rings;
+      bulk_prefetch_l2(a.in + ((size_t)ns * a.n_rings + nta) * nb, (nvb ? 2u : 1u) * nb * 16u);
+    }
   }
   __syncthreads();
   mbar_wait(mb, 0);
@@ -1037,7 +1059,14 @@ __global__ void __launch_bounds__(T, 2) theta_syn_k2_kernel(ThetaSynArgs a) {
   const FftTablesDev& F = a.T;
   const int tid = threadIdx.x;
   const ThetaSynRow R = theta_syn_row(a, blockIdx.x, true);
-  if (tid == 0) k2_issue(mb, tw, F.tw12, buf, R.ge, R.go);
+  if (tid == 0) {
+    k2_issue(mb, tw, F.tw12, buf, R.ge, R.go);
+    if (a.pfd && blockIdx.x + a.pfd < gridDim.x) {
+      const ThetaSynRow Rn = theta_syn_row(a, blockIdx.x + a.pfd, true);
+      if (Rn.ge) bulk_prefetch_l2(Rn.ge, K2_K * 16u);
+      if (Rn.go) bulk_prefetch_l2(Rn.go, K2_K * 16u);
+    }
+  }
   __syncthreads();
   mbar_wait(mb, 0);
   // 1. parity extension on the 2k analysis points
@@ -1080,7 +1109,7 @@ __global__ void __launch_bounds__(T, 2) theta_syn_k2_kernel(ThetaSynArgs a) {
 }
 
 template <int T>
-__global__ void __launch_bounds__(T, 2) theta_k2_kernel(ThetaArgs a) {
+__global__ void __launch_bounds__(T, T >= 512 ? 1 : 2) theta_k2_kernel(ThetaArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   double2* buf = smem;               // [4096]
   double2* side = smem + K2_M;       // [2048]
@@ -1095,7 +1124,14 @@ __global__ void __launch_bounds__(T, 2) theta_k2_kernel(ThetaArgs a) {
     const ThetaPair P = theta_pair(a, blockIdx.x, true);
     has_e = P.ge != nullptr;
     has_o = P.go != nullptr;
-    if (tid == 0) k2_issue(mb, tw, F.tw12, buf, P.ge, P.go);
+    if (tid == 0) {
+      k2_issue(mb, tw, F.tw12, buf, P.ge, P.go);
+      if (a.pfd && blockIdx.x + a.pfd < gridDim.x) {
+        const ThetaPair Pn = theta_pair(a, blockIdx.x + a.pfd, true);
+        if (Pn.ge) bulk_prefetch_l2(Pn.ge, K2_K * 16u);
+        if (Pn.go) bulk_prefetch_l2(Pn.go, K2_K * 16u);
+      }
+    }
   }
   __syncthreads();
   mbar_wait(mb, 0);
@@ -1297,10 +1333,15 @@ static size_t k2_smem(int side, bool tw) {
   return ((size_t)K2_M + side + (tw ? K2_NTW : 0)) * sizeof(double2) + 16;
 }
 template <class Args>
-static cudaError_t k2_launch(void (*kern)(Args), Args a, int n_rows, size_t smem, cudaStream_t st) {
+static cudaError_t k2_launch(void (*kern)(Args), Args a, int n_rows, size_t smem, cudaStream_t st,
+                             int threads = K2_T) {
   cudaError_t e = set_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
-  kern<<<n_rows, K2_T, smem, st>>>(a);
+  static const bool no_pf = getenv("S2W_K2_NOPF") != nullptr;
+  int per_sm = 0;
+  if (!no_pf && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) == cudaSuccess)
+    a.pfd = per_sm * device_sms();
+  kern<<<n_rows, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 // bulk copies need 16-byte aligned rows: complex buffers always are (if the
@@ -1356,7 +1397,7 @@ cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
   if (use_pfa(a.T.N) && a.T.tw12 && k2_ok(a.in, false, 0))
-    return k2_launch(theta_k2_kernel<K2_T>, a, n_rows, k2_smem(K2_K, true), st);
+    return k2_launch(theta_k2_kernel<K2_TT>, a, n_rows, k2_smem(K2_K, true), st, K2_TT);
   if (use_pfa(a.T.N) && a.T.logM == 13) return row_launch(theta_kernel<13, true>, 13, a, n_rows, st);
   S2W_FFT_DISPATCH(theta_kernel, theta_split_kernel, a, n_rows, st)
 }

@@ -167,10 +167,14 @@ S2W_DEV void pfa_pass(double2* __restrict__ buf, int tid, int nthr) {
   }
 }
 
-// Slot of output bin k after pfa4095.
-S2W_DEV int pfa_pos(int k) {
-  const int p = 315 * (k % 13) + 585 * (k % 7) + 819 * (k % 5) + 455 * (k % 9);
-  return p % PFA_N;
+// Slot of output bin k after pfa4095: sum_i (k mod P_i)(N/P_i) mod N, and
+// since P_i (N/P_i) = N that is k * sum_i N/P_i = 2174 k (mod N).  Additive:
+// pfa_pos(k + d) = pfa_pos(k) + pfa_pos(d) (mod N).
+constexpr int PFA_STEP = 315 + 585 + 819 + 455;  // 2174
+S2W_DEV int pfa_pos(int k) { return (int)(((unsigned)k * (unsigned)PFA_STEP) % (unsigned)PFA_N); }
+S2W_DEV int pfa_next(int pos, int dpos) {
+  const int p = pos + dpos;
+  return p >= PFA_N ? p - PFA_N : p;
 }
 
 // Unnormalised DFT_4095 of buf[0..4095) (natural order in, pfa_pos order out).

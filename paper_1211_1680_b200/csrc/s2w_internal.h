@@ -51,6 +51,7 @@ struct PhiFwdArgs {
   double scale;
   int gsize, rpc;  // filled by the launcher
   double2* scratch;  // split mode: per-CTA scratch (fft_split_scratch_elems)
+  int pfd = 0;  // k2 kernels: rows ahead whose input a CTA prefetches into L2 (launcher)
 };
 
 struct PhiInvArgs {
@@ -63,6 +64,7 @@ struct PhiInvArgs {
   int gsize, rpc;
   double2* scratch;
   double thresh = 0.0;  // > 0: hard threshold: samples with |value| < thresh are zeroed (denoise)
+  int pfd = 0;  // k2 kernels: rows ahead whose input a CTA prefetches into L2 (launcher)
 };
 
 // The theta operator commutes with the reflection theta -> 2 pi - theta, so an
@@ -78,6 +80,7 @@ struct ThetaArgs {
   double2* out;       // [set][mi][k] (may alias in)
   int gsize, rpc;
   double2* scratch;
+  int pfd = 0;  // k2 kernels: rows ahead whose input a CTA prefetches into L2 (launcher)
 };
 
 // MW synthesis theta stage: G on the analysis rings theta''_j (m-major) ->
@@ -91,6 +94,7 @@ struct ThetaSynArgs {
   double2* out;       // [set][t][n_bins] (MW rings), must not alias in
   int rpc;
   double2* scratch;
+  int pfd = 0;  // k2 kernels: rows ahead whose input a CTA prefetches into L2 (launcher)
 };
 
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st);
