@@ -85,6 +85,36 @@ def legendre_flops(k, nsets, real):
     return 4.0 * nsets * k * S + 4.0 * k * k * (k + 1) / 2
 
 
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the
+    B200_PROFILING.md fallback."""
+    try:
+        with open(ROOT / "MEASURED_PEAKS.json") as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except (OSError, ValueError, KeyError):
+        return 7700.0, "fallback 7.7 TB/s (B200_PROFILING.md)"
+
+
+def stage_bytes(cfg, bands):
+    """Algorithmic HBM bytes per round trip of the ring-FFT and theta stages
+    (SURVEY 8(d)): one read of the input and one write of the output per SHT.
+    phi: k(2k-1) e + k n_m 16 (e = 8 real / 16 complex map samples; n_m = k
+    real / 2k-1 complex Fourier columns); theta (MW forward) and the MW
+    synthesis resampling (k >= 1024): 2 k n_m 16.  The SHTs of a round trip run
+    at L and at every scale band, once per direction."""
+    B, real = cfg["batch"], cfg["real"]
+    ks = [cfg["L"]] + list(bands)
+    e = 8 if real else 16
+
+    def nm(k):
+        return k if real else 2 * k - 1
+
+    phi = sum(B * (k * (2 * k - 1) * e + k * nm(k) * 16) for k in ks)
+    theta = sum(B * 2 * k * nm(k) * 16 for k in ks)
+    theta += sum(B * 2 * k * nm(k) * 16 for k in ks if k >= 1024)
+    return {"phi_fwd": phi, "phi_inv": phi, "theta": theta}
+
+
 def stage_flops(cfg, bands):
     """Canonical FLOPs per launch of the two grouped Legendre launches of each direction."""
     L, B, real = cfg["L"], cfg["batch"], cfg["real"]
@@ -353,6 +383,7 @@ def run_ours(args, cfgname):
                            "no FP64 entry",
         },
         "stages": stages,
+        "hbm_stages": hbm_stages(cfg, bands, stages),
         "canonical_flops_per_rt": fl["per_rt"],
         "fp64_tflops_per_gpu": fl["per_rt"] * value / ws / 1e12 / B,
         "rt_rel_err": err,
@@ -362,6 +393,19 @@ def run_ours(args, cfgname):
     if dist.is_initialized():
         dist.destroy_process_group()
     return rec
+
+
+def hbm_stages(cfg, bands, stages):
+    """Achieved HBM bandwidth of the ring-FFT / theta stages: algorithmic bytes
+    per round trip (stage_bytes) / the stage's CUDA-event time per round trip."""
+    peak, src = hbm_peak_gbs()
+    out = {"peak_gbs": peak, "peak_source": src}
+    for name, nb in stage_bytes(cfg, bands).items():
+        ms = stages.get(name, {}).get("ms_per_step", 0.0)
+        gbs = nb / (ms * 1e-3) / 1e9 if ms else None
+        out[name] = {"bytes_per_rt": nb, "ms_per_rt": ms, "gbs": gbs,
+                     "frac": gbs / peak if gbs else None}
+    return out
 
 
 def cpu_baseline(cfgname, args):

@@ -25,6 +25,13 @@
 
 namespace s2w {
 
+// resident CTAs per SM the row kernels are compiled for (register cap):
+// two for the 4096-point rows (k = 729 .. 1024 class grids), else one
+#ifndef S2W_ROW_MINB12
+#define S2W_ROW_MINB12 2
+#endif
+__host__ __device__ constexpr int fft_minb(int logm) { return (logm >= 10 && logm <= 12) ? S2W_ROW_MINB12 : 1; }
+
 __device__ __forceinline__ double2 load_map_elem(const double* __restrict__ in, long long idx,
                                                  int real) {
   if (real) return make_double2(__ldg(&in[idx]), 0.0);
@@ -40,7 +47,7 @@ S2W_DEV double2 hard_thresh(double2 v, double t) {
 
 // ---------------------------------------------------------------- phi forward
 template <int LOGM>
-__global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_fwd_kernel(PhiFwdArgs a) {
+__global__ void __launch_bounds__(fft_maxthr(LOGM), fft_minb(LOGM)) phi_fwd_kernel(PhiFwdArgs a) {
   // Real maps: two rings per transform (z = x + i y; X_k = (Z_k + conj Z_{N-k})/2,
   // Y_k = (Z_k - conj Z_{N-k})/2i), halving the FFT work.
   extern __shared__ double2 smem[];
@@ -101,7 +108,7 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_fwd_kernel(PhiFwdArgs a)
 
 // ---------------------------------------------------------------- phi inverse
 template <int LOGM>
-__global__ void __launch_bounds__(fft_maxthr(LOGM)) phi_inv_kernel(PhiInvArgs a) {
+__global__ void __launch_bounds__(fft_maxthr(LOGM), fft_minb(LOGM)) phi_inv_kernel(PhiInvArgs a) {
   // Real maps: two rings per transform (Z = X + i Y of their Hermitian spectra;
   // the two real rings are Re and Im of the inverse DFT).
   extern __shared__ double2 smem[];
@@ -312,7 +319,7 @@ S2W_DEV void theta_store(const ThetaPair& P, const ThetaArgs& a, int t, double2 
 // PFA: N = 4095, the DFT_N of step 2 runs on the prime-factor engine
 // (natural order in the first 4095 slots, no chirps).
 template <int LOGM, bool PFA = false>
-__global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_kernel(ThetaArgs a) {
+__global__ void __launch_bounds__(fft_maxthr(LOGM), fft_minb(LOGM)) theta_kernel(ThetaArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
   constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
@@ -482,7 +489,7 @@ S2W_DEV void theta_syn_store(const ThetaSynRow& R, const ThetaSynArgs& a, int t,
 
 // PFA: N = 4095, the inverse DFT_N of step 4 runs on the prime-factor engine.
 template <int LOGM, bool PFA = false>
-__global__ void __launch_bounds__(fft_maxthr(LOGM)) theta_syn_kernel(ThetaSynArgs a) {
+__global__ void __launch_bounds__(fft_maxthr(LOGM), fft_minb(LOGM)) theta_syn_kernel(ThetaSynArgs a) {
   extern __shared__ double2 smem[];
   const FftTablesDev& T = a.T;
   constexpr int M = 1 << LOGM, GS = fft_gs(LOGM);
