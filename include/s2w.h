@@ -143,6 +143,12 @@ int s2w_wav_denoise_pixel(s2w_wav_plan* plan, const double* map, const double* t
  * s2w_wav_synthesis_pixel the recombined f_lm (transform.py:196-200). */
 int s2w_wav_plan_flm(s2w_wav_plan* plan, double** flm);
 
+/* Per-scale ring stages (phi and theta of each scale map) run concurrently on
+ * plan-owned side streams forked from and joined back into the caller's
+ * stream (default, on != 0), or in order on the caller's stream (on == 0:
+ * serial per-stage profiling).  Results are bit-identical either way. */
+int s2w_wav_plan_set_concurrency(s2w_wav_plan* plan, int on);
+
 /* ---------------------------------------------------------------- S2WM files (mapio.py) */
 /* 22-byte little-endian header (mapio.py:1-15): magic, version, scheme, L, kind, count.
  * Validates length, magic and version (mapio.py:110-119); the caller checks kind,

@@ -37,6 +37,7 @@ _PROTOS = {
     ),
     "s2w_wav_plan_destroy": (_c_int, [_vp]),
     "s2w_wav_plan_flm": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "s2w_wav_plan_set_concurrency": (_c_int, [_vp, _c_int]),
     "s2w_wav_analysis_harmonic": (_c_int, [_vp, _c_int, _vp, ctypes.POINTER(_vp), _vp]),
     "s2w_wav_synthesis_harmonic": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_wav_analysis_pixel": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),

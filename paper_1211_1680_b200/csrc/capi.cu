@@ -12,6 +12,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -1163,6 +1164,45 @@ struct s2w_wav_plan {
   SynthCfg syn_top, syn_scales;
   AnaCfg ana_top, ana_scales;
   double2* bufs() const { return nullptr; }
+  // Per-scale ring stages (phi / theta of each scale map) are independent:
+  // they run on side streams forked from and joined back into the caller's
+  // stream (event fork/join, so CUDA-graph capture follows them), largest
+  // band first, each scale with its own resampling target and each side
+  // stream with its own split-mode scratch.
+  static constexpr int NSIDE = 4;
+  bool concurrent = true;
+  cudaStream_t side[NSIDE] = {};
+  cudaEvent_t fork = nullptr, join[NSIDE] = {};
+  std::vector<int> order;                 // scales by descending band
+  std::vector<std::unique_ptr<DevBuf>> Grj;  // per scale resampling target (MW, k >= 1024)
+  DevBuf sscratch[NSIDE];
+  ~s2w_wav_plan() {
+    for (int i = 0; i < NSIDE; ++i) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (join[i]) cudaEventDestroy(join[i]);
+    }
+    if (fork) cudaEventDestroy(fork);
+  }
+  // run f(j, stream, scratch, Gr_j) for every scale on the side streams
+  template <class F>
+  int per_scale(cudaStream_t st, F&& f) {
+    if (!concurrent) {
+      for (int j : order) CHECK(f(j, st, sscratch[0].as<double2>(), Grj[j] ? Grj[j]->as<double2>() : nullptr));
+      return S2W_OK;
+    }
+    CU(cudaEventRecord(fork, st));
+    const int ns = std::min<int>(NSIDE, (int)order.size());
+    for (int i = 0; i < ns; ++i) CU(cudaStreamWaitEvent(side[i], fork, 0));
+    for (size_t i = 0; i < order.size(); ++i) {
+      const int j = order[i], q = (int)(i % NSIDE);
+      CHECK(f(j, side[q], sscratch[q].as<double2>(), Grj[j] ? Grj[j]->as<double2>() : nullptr));
+    }
+    for (int i = 0; i < ns; ++i) {
+      CU(cudaEventRecord(join[i], side[i]));
+      CU(cudaStreamWaitEvent(st, join[i], 0));
+    }
+    return S2W_OK;
+  }
 };
 
 extern "C" {
@@ -1220,6 +1260,27 @@ int s2w_wav_plan_create(int scheme, int L, int batch, int is_real, int n_kern,
     return bail(r);
   if ((r = p->scratch.ensure(sizeof(double2) * fft_split_scratch_elems(p->top->logM))) != S2W_OK)
     return bail(r);
+  // side streams, per-scale resampling targets and per-stream scratch
+  for (int i = 0; i < s2w_wav_plan::NSIDE; ++i) {
+    if (cudaStreamCreateWithFlags(&p->side[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->join[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(S2W_ECUDA, "side stream / event creation failed"));
+    if ((r = p->sscratch[i].ensure(sizeof(double2) * fft_split_scratch_elems(p->top->logM))) != S2W_OK)
+      return bail(r);
+  }
+  if (cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(S2W_ECUDA, "event creation failed"));
+  for (int j = 0; j < n_kern; ++j) p->order.push_back(j);
+  std::stable_sort(p->order.begin(), p->order.end(),
+                   [&](int a, int b) { return p->bands[a] > p->bands[b]; });
+  p->Grj.resize(n_kern);
+  for (int j = 0; j < n_kern; ++j) {
+    const GridRes* g = p->kgrid[j];
+    if (!g->syn_on_ana()) continue;
+    p->Grj[j].reset(new DevBuf());
+    if ((r = p->Grj[j]->ensure(sizeof(double2) * (size_t)batch * g->n_bins(cplx) * g->k)) != S2W_OK)
+      return bail(r);
+  }
 
   // slots: 0 = f, 1 = Gtop, 2 = Gs
   const int nbL = p->top->n_bins(cplx);
@@ -1300,6 +1361,12 @@ int s2w_wav_plan_destroy(s2w_wav_plan* plan) {
   if (!plan) return S2W_OK;
   DeviceGuard dg(plan->device);
   delete plan;
+  return S2W_OK;
+}
+
+int s2w_wav_plan_set_concurrency(s2w_wav_plan* p, int on) {
+  if (!p) return fail(S2W_EPARAM, "null argument");
+  p->concurrent = on != 0;
   return S2W_OK;
 }
 
@@ -1393,11 +1460,10 @@ static int wav_analysis_pixel_impl(s2w_wav_plan* p, const double* map, const dou
   CHECK(run_synth(p->syn_scales, p->top->seed_c, bufs, st));
   // hard thresholding of the wavelet maps (not the scaling map) fused into
   // the ring-DFT epilogue (denoise.py:78-96)
-  for (int j = 0; j < p->nk; ++j)
-    CHECK(inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
-                        p->scratch.as<double2>(), p->Gr.as<double2>(), st,
-                        (thresholds && j > 0) ? thresholds[j] : 0.0));
-  return S2W_OK;
+  return p->per_scale(st, [&](int j, cudaStream_t s, double2* scratch, double2* Gr) {
+    return inverse_rings(p->kgrid[j], p->B, !cplx, p->Gs.as<double2>() + p->goff[j], scale_maps[j],
+                         scratch, Gr, s, (thresholds && j > 0) ? thresholds[j] : 0.0);
+  });
 }
 
 int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, double* map,
@@ -1410,9 +1476,10 @@ int s2w_wav_synthesis_pixel(s2w_wav_plan* p, const double* const* scale_maps, do
   double2* bufs[S2W_NBUF] = {p->f.as<double2>(), p->Gtop.as<double2>(), p->Gs.as<double2>(),
                              nullptr};
   // per-scale analysis (transform.py:196)
-  for (int j = 0; j < p->nk; ++j)
-    CHECK(forward_rings(p->kgrid[j], p->B, !cplx, scale_maps[j], p->Gs.as<double2>() + p->goff[j],
-                        p->scratch.as<double2>(), st));
+  CHECK(p->per_scale(st, [&](int j, cudaStream_t s, double2* scratch, double2*) {
+    return forward_rings(p->kgrid[j], p->B, !cplx, scale_maps[j], p->Gs.as<double2>() + p->goff[j],
+                         scratch, s);
+  }));
   CU(cudaMemsetAsync(p->f.p, 0, sizeof(double2) * (size_t)p->B * p->L * p->L, st));
   // recombination (transform.py:197-199) fused into the analysis reduction
   CHECK(run_ana(p->ana_scales, p->top->seed_c, bufs, st));

@@ -79,6 +79,11 @@ class WaveletTransform:
         th = _device.torch()
         return th.float64 if self.real else th.complex128
 
+    def set_concurrency(self, on: bool) -> None:
+        """Per-scale ring stages on forked side streams (default) or serially on
+        the caller's stream (per-stage profiling); results are identical."""
+        _native.check(_native.load().s2w_wav_plan_set_concurrency(self.plan.handle, int(bool(on))))
+
     def alloc_scale_maps(self):
         th = _device.torch()
         return [th.empty((self.batch, g.n_theta, g.n_phi), dtype=self._dtype(),
