@@ -1,0 +1,200 @@
+// The MW theta stage pieces shared by fft_kernels.cu (theta kernels) and
+// legendre_kernels.cu (the Legendre analysis with the theta stage fused in):
+// parity pairs of theta columns and the N = 4095 (L = 2048) column-pair
+// transform theta_k2_row (see fft_kernels.cu, "k2").
+#pragma once
+#include "fft.cuh"
+#include "pfa.cuh"
+#include "s2w_internal.h"
+
+namespace s2w {
+
+// ---------------------------------------------------------------- MW theta stage
+// Parity pairing: the operator (extension -> band-limited |sin| product ->
+// first k rings) commutes with the reflection R: n -> N-1-n.  An even-m row
+// x is extended evenly, an odd-m row y oddly, except at the pole sample n=k-1
+// (its own mirror) where both keep their value.  So z = x~ + y~ is transformed
+// once and split: with delta = y(k-1) and r = response to a unit pole sample
+// (even), the even part of the result is H_x + delta r and the odd part is
+// H_y - delta r.
+struct ThetaPair {
+  const double2* ge;  // even-m input row (nullptr: none)
+  const double2* go;  // odd-m input row
+  double2* he;
+  double2* ho;
+  double2 delta;      // odd row's pole sample
+};
+
+S2W_DEV ThetaPair theta_pair(const ThetaArgs& a, int row, bool valid) {
+  ThetaPair P{nullptr, nullptr, nullptr, nullptr, make_double2(0.0, 0.0)};
+  if (!valid) return P;
+  const int set = row / a.n_pairs, pi = row - set * a.n_pairs;
+  const int2 pr = a.pairs[pi];
+  const size_t base = (size_t)set * a.n_bins;
+  if (pr.x >= 0) {
+    P.ge = a.in + (base + pr.x) * a.k;
+    P.he = a.out + (base + pr.x) * a.k;
+  }
+  if (pr.y >= 0) {
+    P.go = a.in + (base + pr.y) * a.k;
+    P.ho = a.out + (base + pr.y) * a.k;
+    P.delta = __ldg(&P.go[a.k - 1]);
+  }
+  return P;
+}
+
+// extended sample n < N of the paired row
+S2W_DEV double2 theta_ext(const ThetaPair& P, int n, int k) {
+  const bool lo = n < k;
+  const int src = lo ? n : 2 * k - 2 - n;
+  const double2 e = P.ge ? __ldg(&P.ge[src]) : make_double2(0.0, 0.0);
+  const double2 o = P.go ? __ldg(&P.go[src]) : make_double2(0.0, 0.0);
+  return lo ? cadd(e, o) : csub(e, o);
+}
+
+// write ring t < k from w_t = result(t), w_r = result(N-1-t)
+S2W_DEV void theta_store(const ThetaPair& P, const ThetaArgs& a, int t, double2 wt, double2 wr) {
+  const double2 r = a.pole_resp ? __ldg(&a.pole_resp[t]) : make_double2(0.0, 0.0);
+  const double2 dr = cmul(P.delta, r);
+  if (P.he) P.he[t] = csub(cscale(cadd(wt, wr), 0.5), dr);
+  if (P.ho) P.ho[t] = cadd(cscale(csub(wt, wr), 0.5), dr);
+}
+
+
+constexpr int K2_N = 4095, K2_M = 4096, K2_K = 2048;
+constexpr int K2_NTW = 272;  // fft_ntw(12)
+static_assert(K2_NTW == fft_ntw(12), "4096-point pass twiddles");
+
+constexpr size_t k2_theta_smem_bytes() { return ((size_t)K2_M + K2_K + K2_NTW) * 16 + 16; }
+
+// Arm the barrier and issue the bulk copies of the 4096-point pass twiddles
+// and a theta column pair (ge -> dst[0, k), go -> dst[k, 2k)).
+S2W_DEV void k2_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* dst, const double2* ge,
+                      const double2* go) {
+  constexpr unsigned col = K2_K * 16u;
+  mbar_init(mb, 1);
+  mbar_expect_tx(mb, K2_NTW * 16u + (ge ? col : 0u) + (go ? col : 0u));
+  bulk_g2s(tw, gtw, K2_NTW * 16u, mb);
+  if (ge) bulk_g2s(dst, ge, col, mb);
+  if (go) bulk_g2s(dst + K2_K, go, col, mb);
+}
+
+// One theta column pair (row `row` of a) on the CTA's T threads.  smem:
+// k2_theta_smem_bytes() of 16-byte aligned shared memory.  pf > 0: also
+// prefetch row + pf into L2.  Precondition: every thread is done with smem
+// (a barrier) and, if smem held generic-proxy writes, each writer executed
+// fence_proxy_async() before that barrier.  Ends with the stores issued.
+template <int T>
+S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
+  double2* buf = smem;               // [4096]
+  double2* side = smem + K2_M;       // [2048]
+  double2* tw = side + K2_K;         // [272]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(tw + K2_NTW);
+  constexpr int N = K2_N, k = K2_K, U = K2_M / T, V = K2_K / T;
+  const FftTablesDev& F = a.T;
+  const int tid = threadIdx.x;
+  bool has_e, has_o;
+  {
+    // (the pair is re-read for the stores: nothing stays live across the FFTs)
+    const ThetaPair P = theta_pair(a, row, true);
+    has_e = P.ge != nullptr;
+    has_o = P.go != nullptr;
+    if (tid == 0) {
+      k2_issue(mb, tw, F.tw12, buf, P.ge, P.go);
+      if (pf) {
+        const ThetaPair Pn = theta_pair(a, row + pf, true);
+        if (Pn.ge) bulk_prefetch_l2(Pn.ge, K2_K * 16u);
+        if (Pn.go) bulk_prefetch_l2(Pn.go, K2_K * 16u);
+      }
+    }
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  // 1. parity extension to the full circle (natural order for the PFA)
+  double2 x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 2 - n;
+    const double2 e = (has_e && n < N) ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = (has_o && n < N) ? buf[k + src] : make_double2(0.0, 0.0);
+    x[u] = lo ? cadd(e, o) : csub(e, o);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    if (n < N) buf[n] = x[u];
+  }
+  __syncthreads();
+  // 2. DFT_N
+  pfa4095<false>(buf, tid, T);
+  // 3. Fourier coefficients a_q = X_bin e^{-i pi q/N} / N by parity of q:
+  //    even q = 2b -> buf slot b (mod 4096), odd q = 2b+1 -> side slot b (mod 2048)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    x[u] = bin < N ? cmul(buf[pfa_pos(bin)], __ldg(&F.phA[bin])) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    if (bin >= N) continue;
+    const int q = bin < k ? bin : bin - N;
+    if (q & 1) side[((q - 1) >> 1) & (K2_K - 1)] = x[u];
+    else buf[swz((q >> 1) & (K2_M - 1))] = x[u];
+  }
+  for (int s = 1024 + tid; s <= 3072; s += T) buf[swz(s)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
+  //      a); in between, even outputs -> side, odd coefficients -> buf
+#pragma unroll 1
+  for (int cls = 0; cls < 2; ++cls) {
+    fft_conv_real<12, T>(buf, tw, F.w2s, tid);
+    if (cls) break;
+    double2 ev[V], od[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 1024 ? i : i - 2048;
+      ev[u] = buf[swz(aa & (K2_M - 1))];
+      od[u] = side[aa & (K2_K - 1)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 1024 ? i : i - 2048;
+      buf[swz(aa & (K2_M - 1))] = od[u];
+      side[aa & (K2_K - 1)] = ev[u];
+      buf[swz(1024 + i)] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+  // 7. evaluation on the analysis rings: X'_n = conj(H'(q)) e^{-i pi q/N2}, n = q mod N2
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const int q = n < k ? n : n - K2_M;
+    double2 h = make_double2(0.0, 0.0);
+    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (K2_M - 1))] : side[(q >> 1) & (K2_K - 1)];
+    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  __syncthreads();
+  // 8. direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
+  fft_fwd<12, T, 0>(buf, tw, tid);
+  const ThetaPair P = theta_pair(a, row, true);
+  for (int t = tid; t < k; t += T) {
+    const double2 wt = cconj(buf[swz(fft_brev<12>(t))]);
+    const double2 wr = cconj(buf[swz(fft_brev<12>(K2_M - 1 - t))]);
+    theta_store(P, a, t, wt, wr);
+  }
+}
+
+
+}  // namespace s2w
