@@ -358,8 +358,10 @@ struct GridRes {
   double2 *tw = nullptr, *octM = nullptr, *chirp = nullptr, *bl_fwd = nullptr, *bl_inv = nullptr,
           *ph1 = nullptr, *ph2 = nullptr, *wconv = nullptr, *chirp2 = nullptr, *bl_ev = nullptr,
           *bl_fwd2 = nullptr, *ph4 = nullptr, *ph2d = nullptr, *ph4d = nullptr, *tw12 = nullptr,
-          *phA = nullptr, *phS = nullptr;
+          *phA = nullptr, *phS = nullptr, *rD = nullptr;
   double* w2s = nullptr;
+  double* w4s = nullptr;
+  int *rgpow = nullptr, *rplog = nullptr;
   double* seed_c = nullptr;
   // MW theta stage: parity pairs of the full real / complex bin layouts, pole response
   int2 *pairs_r = nullptr, *pairs_c = nullptr;
@@ -400,6 +402,10 @@ struct GridRes {
     t.w2s = w2s;
     t.phA = phA;
     t.phS = phS;
+    t.rgpow = rgpow;
+    t.rplog = rplog;
+    t.rD = rD;
+    t.w4s = w4s;
     return t;
   }
   // MW synthesis runs on the (symmetric) analysis rings and is resampled to
@@ -706,6 +712,67 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     std::vector<double> w2r;
     for (const double2& z : spectrum_brev(w2)) w2r.push_back(z.x);  // Im ~ 1e-19: exact zero
     CHECK(upload_new(&g->w2s, w2r));
+    CHECK(upload_new(&g->phA, phA));
+    CHECK(upload_new(&g->phS, phS));
+  }
+  if (N == 8191) {
+    // k4 stage kernels: Rader's DFT_8191 over the prime-factor DFT_8190
+    // (pfa.cuh), the |sin| series on one parity class at M = 8192, and the
+    // theta / theta_syn bin phases
+    const int R = 8190, G = 17, STEP = 253, M4 = 8192;
+    std::vector<int> gpow(R), plog(N, 0);
+    long long gq = 1;
+    for (int q = 0; q < R; ++q) {
+      gpow[q] = (int)gq;
+      gq = gq * G % N;
+    }
+    long long ginv = 1;  // G^(N-2) mod N
+    for (int e = 0; e < N - 2; ++e) ginv = ginv * G % N;
+    std::vector<cld> dd(R);
+    long long gi = 1;  // g^-j
+    for (int j = 0; j < R; ++j) {
+      plog[gi] = j;
+      const ld ang = -2.0L * PI_L * (ld)gi / (ld)N;
+      dd[j] = cld(std::cos(ang), std::sin(ang));
+      gi = gi * ginv % N;
+    }
+    // DFT_8190 of d in long double (direct O(R log R) via the radix-2 long
+    // double FFT would need a power of two: use the exact O(R^2) sum, once per grid)
+    std::vector<double2> Dslot(R);
+    {
+      std::vector<cld> tw(R);
+      for (int t = 0; t < R; ++t) {
+        const ld ang = -2.0L * PI_L * (ld)t / (ld)R;
+        tw[t] = cld(std::cos(ang), std::sin(ang));
+      }
+      for (int kk = 0; kk < R; ++kk) {
+        cld acc(0, 0);
+        long long idx = 0;
+        for (int j = 0; j < R; ++j) {
+          acc += dd[j] * tw[idx];
+          idx += kk;
+          if (idx >= R) idx -= R;
+        }
+        Dslot[(long long)kk * STEP % R] = d2(acc / (ld)R);
+      }
+    }
+    std::vector<cld> w4(M4, cld(0, 0));
+    for (int d = -(M4 / 2 - 1); d <= M4 / 2 - 1; ++d)
+      w4[(d + M4) % M4] = cld(4.0L / (1.0L - 4.0L * (ld)d * (ld)d), 0);
+    std::vector<double> w4r;
+    for (const double2& z : spectrum_brev(w4)) w4r.push_back(z.x);  // Im ~ 1e-19: exact zero
+    std::vector<double2> phA(N), phS(N);
+    for (int n = 0; n < N; ++n) {
+      const int q = n < k ? n : n - N;
+      const ld a1 = -PI_L * (ld)q / (ld)N;
+      phA[n] = d2(cld(std::cos(a1), std::sin(a1)) / (ld)N);
+      const ld a2 = -PI_L * (ld)q / (ld)N2 + PI_L * (ld)q / (ld)N;
+      phS[n] = d2(cld(std::cos(a2), std::sin(a2)) / (ld)N2);
+    }
+    CHECK(upload_new(&g->rgpow, gpow));
+    CHECK(upload_new(&g->rplog, plog));
+    CHECK(upload_new(&g->rD, Dslot));
+    CHECK(upload_new(&g->w4s, w4r));
     CHECK(upload_new(&g->phA, phA));
     CHECK(upload_new(&g->phS, phS));
   }

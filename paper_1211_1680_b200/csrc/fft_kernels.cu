@@ -1057,6 +1057,322 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : 2) theta_k2_kernel(ThetaArgs
   theta_k2_row<T>(a, blockIdx.x, smem, pf);
 }
 
+// =====================================================================
+// k4: the N = 8191 (L = 4096) stages.  8191 is prime: Rader's algorithm over
+// the prime-factor DFT_8190 (pfa.cuh) replaces the 16384-point Bluestein
+// convolutions of split mode, so a row fits shared memory (128 KiB + the theta
+// side buffer): one CTA of 512 threads per SM, the row loaded by one bulk copy.
+//  * phi_fwd_k4 / phi_inv_k4: ring DFTs (same I/O as phi_fwd/inv_kernel).
+//  * theta_syn_k4: direct 8192-point FFT + Rader inverse DFT_8191.
+//  * theta_k4: Rader DFT_8191, the |sin| convolution on the two parity
+//    classes of the Fourier index (two 8192-point real-spectrum convolutions,
+//    as theta_k2), evaluation by a direct 8192-point FFT.
+// =====================================================================
+constexpr int K4_N = 8191, K4_M = 8192, K4_K = 4096;
+#ifndef S2W_K4_T
+#define S2W_K4_T 512
+#endif
+constexpr int K4_T = S2W_K4_T;
+constexpr int K4_NTW = 546;  // fft_ntw(13)
+static_assert(K4_NTW == fft_ntw(13), "8192-point pass twiddles");
+
+S2W_DEV RaderTabs rader_tabs(const FftTablesDev& F) { return RaderTabs{F.rgpow, F.rplog, F.rD}; }
+
+template <int T>
+__global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;                 // [8192]
+  double2* part = smem + K4_M;         // [T/32]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
+  constexpr int N = K4_N, U = (K4_N + T - 1) / T;
+  const int tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const long long base_a = ((long long)set * a.n_rings + ta) * N;
+  const unsigned bytes = a.real ? 2u * N * 8u : N * 16u;  // real rows come in pairs (launcher)
+  if (tid == 0) {
+    mbar_init(mb, 1);
+    mbar_expect_tx(mb, bytes);
+    bulk_g2s(buf, a.in + (a.real ? base_a : 2 * base_a), bytes, mb);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  if (a.real) {
+    const double* r = reinterpret_cast<const double*>(buf);
+    double xr[U], xi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      xr[u] = n < N ? r[n] : 0.0;
+      xi[u] = (n < N && vb) ? r[N + n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      if (n < N) buf[n] = make_double2(xr[u], xi[u]);
+    }
+    __syncthreads();
+  }
+  const RaderTabs R = rader_tabs(a.T);
+  double2 x0, X0;
+  rader8191<T, false>(buf, R, part, x0, X0);
+  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
+  for (int mi = tid; mi < a.n_bins; mi += T) {
+    const double2 z = rader_bin<false>(buf, R, x0, X0, mi);
+    if (!a.real) {
+      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+    } else {
+      const double2 zr = cconj(rader_bin<false>(buf, R, x0, X0, mi ? N - mi : 0));
+      const double h = 0.5 * a.scale;
+      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
+      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 1) phi_inv_k4_kernel(PhiInvArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;
+  double2* part = smem + K4_M;
+  uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
+  constexpr int N = K4_N, U = (K4_N + T - 1) / T;
+  const int tid = threadIdx.x;
+  const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
+  const int row = blockIdx.x;
+  const int set = row / per, p = row - set * per;
+  const int ta = a.real ? 2 * p : p;
+  const bool vb = a.real && ta + 1 < a.n_rings;
+  const int nb = a.n_bins;
+  const double2* Ga = a.in + ((size_t)set * a.n_rings + ta) * nb;
+  const double2* Gb = Ga + nb;
+  const unsigned bytes = (vb ? 2u : 1u) * nb * 16u;
+  if (tid == 0) {
+    mbar_init(mb, 1);
+    mbar_expect_tx(mb, bytes);
+    bulk_g2s(buf, Ga, bytes, mb);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  if (a.real) {
+    double2 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      x[u] = make_double2(0.0, 0.0);
+      if (n < N) {
+        const bool lo = n < nb;
+        const int src = lo ? n : N - n;
+        double2 X = buf[src], Y = vb ? buf[nb + src] : make_double2(0.0, 0.0);
+        if (!lo) {
+          X = cconj(X);
+          Y = cconj(Y);
+        }
+        if (n == 0) X.y = Y.y = 0.0;
+        x[u] = cadd(X, cmul_pi(Y));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n = tid + u * T;
+      if (n < N) buf[n] = x[u];
+    }
+    __syncthreads();
+  }
+  const RaderTabs R = rader_tabs(a.T);
+  double2 x0, X0;
+  rader8191<T, true>(buf, R, part, x0, X0);
+  const int pole_ring = (N + 1) / 2 - 1 - a.t_offset;
+  const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
+  const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
+  const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
+  const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+  for (int q = tid; q < N; q += T) {
+    const double2 v = rader_bin<true>(buf, R, x0, X0, q);
+    if (a.real) {
+      a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
+      if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
+    } else {
+      reinterpret_cast<double2*>(a.out)[ob + q] = hard_thresh(pa ? pva : v, a.thresh);
+    }
+  }
+}
+
+// arm the barrier and issue the 8192-point twiddles and a column pair
+S2W_DEV void k4_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* dst, const double2* ge,
+                      const double2* go) {
+  constexpr unsigned col = K4_K * 16u;
+  mbar_init(mb, 1);
+  mbar_expect_tx(mb, K4_NTW * 16u + (ge ? col : 0u) + (go ? col : 0u));
+  bulk_g2s(tw, gtw, K4_NTW * 16u, mb);
+  if (ge) bulk_g2s(dst, ge, col, mb);
+  if (go) bulk_g2s(dst + K4_K, go, col, mb);
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 1) theta_syn_k4_kernel(ThetaSynArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;               // [8192]
+  double2* tw = smem + K4_M;         // [546]
+  double2* part = tw + K4_NTW;       // [T/32]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
+  constexpr int N = K4_N, k = K4_K, U = K4_M / T;
+  const FftTablesDev& F = a.T;
+  const int tid = threadIdx.x;
+  const ThetaSynRow Rw = theta_syn_row(a, blockIdx.x, true);
+  if (tid == 0) k4_issue(mb, tw, F.tw, buf, Rw.ge, Rw.go);
+  __syncthreads();
+  mbar_wait(mb, 0);
+  double2 x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 1 - n;
+    const double2 e = Rw.ge ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = Rw.go ? buf[k + src] : make_double2(0.0, 0.0);
+    x[u] = lo ? cadd(e, o) : csub(e, o);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  __syncthreads();
+  fft_fwd<13, T, 0>(buf, tw, tid);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    x[u] = make_double2(0.0, 0.0);
+    if (n < N) {
+      const int src = n < k ? n : n + 1;
+      x[u] = cmul(buf[swz(fft_brev<13>(src))], __ldg(&F.phS[n]));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    if (n < N) buf[n] = x[u];
+  }
+  __syncthreads();
+  const RaderTabs R = rader_tabs(F);
+  double2 x0, X0;
+  rader8191<T, true>(buf, R, part, x0, X0);
+  for (int t = tid; t < k; t += T)
+    theta_syn_store(Rw, a, t, rader_bin<true>(buf, R, x0, X0, t), rader_bin<true>(buf, R, x0, X0, N - 1 - t));
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 1) theta_k4_kernel(ThetaArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* buf = smem;               // [8192]
+  double2* side = smem + K4_M;       // [4096]
+  double2* tw = side + K4_K;         // [546]
+  double2* part = tw + K4_NTW;       // [T/32]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
+  constexpr int N = K4_N, k = K4_K, U = K4_M / T, V = K4_K / T;
+  const FftTablesDev& F = a.T;
+  const int tid = threadIdx.x;
+  bool has_e, has_o;
+  {
+    const ThetaPair P = theta_pair(a, blockIdx.x, true);
+    has_e = P.ge != nullptr;
+    has_o = P.go != nullptr;
+    if (tid == 0) k4_issue(mb, tw, F.tw, buf, P.ge, P.go);
+  }
+  __syncthreads();
+  mbar_wait(mb, 0);
+  // 1. parity extension (natural order)
+  double2 x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 2 - n;
+    const double2 e = (has_e && n < N) ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = (has_o && n < N) ? buf[k + src] : make_double2(0.0, 0.0);
+    x[u] = lo ? cadd(e, o) : csub(e, o);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    if (n < N) buf[n] = x[u];
+  }
+  __syncthreads();
+  // 2. DFT_N (Rader)
+  const RaderTabs R = rader_tabs(F);
+  double2 x0, X0;
+  rader8191<T, false>(buf, R, part, x0, X0);
+  // 3. coefficients by parity of q (see theta_k2)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    x[u] = bin < N ? cmul(rader_bin<false>(buf, R, x0, X0, bin), __ldg(&F.phA[bin]))
+                   : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int bin = tid + u * T;
+    if (bin >= N) continue;
+    const int q = bin < k ? bin : bin - N;
+    if (q & 1) side[((q - 1) >> 1) & (K4_K - 1)] = x[u];
+    else buf[swz((q >> 1) & (K4_M - 1))] = x[u];
+  }
+  for (int s2 = 2048 + tid; s2 <= 6144; s2 += T) buf[swz(s2)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // 4-6. even class, swap, odd class
+#pragma unroll 1
+  for (int cls = 0; cls < 2; ++cls) {
+    fft_conv_real<13, T>(buf, tw, F.w4s, tid);
+    if (cls) break;
+    double2 ev[V], od[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 2048 ? i : i - 4096;
+      ev[u] = buf[swz(aa & (K4_M - 1))];
+      od[u] = side[aa & (K4_K - 1)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int i = tid + u * T;
+      const int aa = i < 2048 ? i : i - 4096;
+      buf[swz(aa & (K4_M - 1))] = od[u];
+      side[aa & (K4_K - 1)] = ev[u];
+      buf[swz(2048 + i)] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+  // 7. evaluation input X'_n = conj(H'(q)) e^{-i pi q/N2}
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n = tid + u * T;
+    const int q = n < k ? n : n - K4_M;
+    double2 h = make_double2(0.0, 0.0);
+    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (K4_M - 1))] : side[(q >> 1) & (K4_K - 1)];
+    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  __syncthreads();
+  // 8. direct FFT of length N2 = 8192; rings j and N2-1-j, split by parity
+  fft_fwd<13, T, 0>(buf, tw, tid);
+  const ThetaPair P = theta_pair(a, blockIdx.x, true);
+  for (int t = tid; t < k; t += T) {
+    const double2 wt = cconj(buf[swz(fft_brev<13>(t))]);
+    const double2 wr = cconj(buf[swz(fft_brev<13>(K4_M - 1 - t))]);
+    theta_store(P, a, t, wt, wr);
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 static cudaError_t set_smem(const void* fn, size_t smem) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1187,9 +1503,19 @@ static bool k2_ok(const void* base, bool real_pairs, int n_rings) {
   return !off && ((uintptr_t)base & 15) == 0 && (!real_pairs || (n_rings % 2) == 0);
 }
 
+static size_t k4_smem(int side, bool tw) {
+  return ((size_t)K4_M + side + (tw ? K4_NTW : 0) + K4_T / 32) * sizeof(double2) + 16;
+}
+static bool use_k4(const FftTablesDev& T) {
+  static const bool off = getenv("S2W_NO_K4") != nullptr;
+  return !off && T.N == K4_N && T.rD != nullptr;
+}
+
 cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_k4(a.T) && k2_ok(a.in, a.real, a.n_rings))
+    return k2_launch(phi_fwd_k4_kernel<K4_T>, a, n_rows, k4_smem(0, false), st, K4_T);
   if (use_pfa(a.T.N) && k2_ok(a.in, a.real, a.n_rings))
     return k2_launch(phi_fwd_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
   if (use_pfa(a.T.N)) return pfa_launch(phi_fwd_pfa_kernel, a, n_rows, st);
@@ -1199,6 +1525,8 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
 cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * (a.real ? (a.n_rings + 1) / 2 : a.n_rings);
   if (n_rows == 0) return cudaSuccess;
+  if (use_k4(a.T) && k2_ok(a.in, false, a.n_rings) && a.n_bins <= (a.real ? K4_K : K4_N))
+    return k2_launch(phi_inv_k4_kernel<K4_T>, a, n_rows, k4_smem(0, false), st, K4_T);
   if (use_pfa(a.T.N) && k2_ok(a.in, false, a.n_rings) && a.n_bins <= (a.real ? K2_K : K2_N))
     return k2_launch(phi_inv_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
   if (use_pfa(a.T.N)) return pfa_launch(phi_inv_pfa_kernel, a, n_rows, st);
@@ -1222,6 +1550,8 @@ void theta_pairs(const int* bins, int n_rows, int k, std::vector<int2>& pairs) {
 cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_k4(a.T) && k2_ok(a.in, false, 0))
+    return k2_launch(theta_syn_k4_kernel<K4_T>, a, n_rows, k4_smem(0, true), st, K4_T);
   if (use_pfa(a.T.N) && a.T.tw12 && k2_ok(a.in, false, 0))
     return k2_launch(theta_syn_k2_kernel<K2_T>, a, n_rows, k2_smem(0, true), st);
   if (use_pfa(a.T.N) && a.T.logM == 13)
@@ -1232,6 +1562,8 @@ cudaError_t launch_theta_syn(ThetaSynArgs a, cudaStream_t st) {
 cudaError_t launch_theta(ThetaArgs a, cudaStream_t st) {
   const int n_rows = a.n_sets * a.n_pairs;
   if (n_rows == 0) return cudaSuccess;
+  if (use_k4(a.T) && k2_ok(a.in, false, 0))
+    return k2_launch(theta_k4_kernel<K4_T>, a, n_rows, k4_smem(K4_K, true), st, K4_T);
   if (use_pfa(a.T.N) && a.T.tw12 && k2_ok(a.in, false, 0))
     return k2_launch(theta_k2_kernel<K2_TT>, a, n_rows, k2_smem(K2_K, true), st, K2_TT);
   if (use_pfa(a.T.N) && a.T.logM == 13) return row_launch(theta_kernel<13, true>, 13, a, n_rows, st);

@@ -147,24 +147,42 @@ S2W_DEV void dft_odd(double2* v) {
   }
 }
 
-// One axis pass: every line of axis P (stride N/P) through dft_odd.
+// DFT of length P in registers: the conjugate-pair form for odd P, the
+// butterfly for P = 2.
 template <int P, bool INV>
-S2W_DEV void pfa_pass(double2* __restrict__ buf, int tid, int nthr) {
-  constexpr int A = PFA_N / P;  // also the number of lines
+S2W_DEV void dft_p(double2* v) {
+  if constexpr (P == 2) {
+    const double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else {
+    dft_odd<P, INV>(v);
+  }
+}
+
+// One axis pass of a length-NN prime-factor DFT: every line of axis P
+// (slots (P r + j NN/P) mod NN) through dft_p.
+template <int NN, int P, bool INV>
+S2W_DEV void pfa_pass_n(double2* __restrict__ buf, int tid, int nthr) {
+  constexpr int A = NN / P;  // also the number of lines
   for (int r = tid; r < A; r += nthr) {
     double2 v[P];
     int idx[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       int i = P * r + j * A;
-      if (i >= PFA_N) i -= PFA_N;
+      if (i >= NN) i -= NN;
       idx[j] = i;
       v[j] = buf[i];
     }
-    dft_odd<P, INV>(v);
+    dft_p<P, INV>(v);
 #pragma unroll
     for (int j = 0; j < P; ++j) buf[idx[j]] = v[j];
   }
+}
+template <int P, bool INV>
+S2W_DEV void pfa_pass(double2* __restrict__ buf, int tid, int nthr) {
+  pfa_pass_n<PFA_N, P, INV>(buf, tid, nthr);
 }
 
 // Slot of output bin k after pfa4095: sum_i (k mod P_i)(N/P_i) mod N, and
@@ -189,4 +207,87 @@ S2W_DEV void pfa4095(double2* buf, int tid, int nthr) {
   __syncthreads();
   pfa_pass<9, INV>(buf, tid, nthr);
   __syncthreads();
+}
+
+// ------------------------------------------------------------------ N = 8191 (L = 4096)
+// 8191 is prime, so its DFT is Rader's: with the primitive root g = 17,
+//     X_0 = sum_n x_n,   X_{g^-p} = x_0 + sum_q x_{g^q} w^{g^(q-p)},
+// the second term a cyclic convolution of length 8190 = 2 * 9 * 5 * 7 * 13
+// (a_q = x_{g^q} with d_j = w^{g^-j}), done by the prime-factor engine:
+// forward PFA_8190 (natural order in, bin k at slot 253 k mod 8190 out),
+// product with the precomputed spectrum of d stored in that slot order (and
+// divided by 8190), inverse PFA_8190 (slot order in, natural order out).
+// No permutation passes: the input gather g^q and the output map
+// bin g^-p -> p are table lookups.  The inverse DFT is conj(DFT(conj x)).
+constexpr int RADER_N = 8191, RADER_M = 8190, RADER_G = 17;
+constexpr int RADER_STEP = 4095 + 910 + 1638 + 1170 + 630 - RADER_M;  // 253: slot of bin k = 253 k
+
+template <bool INV>
+S2W_DEV void pfa8190(double2* buf, int tid, int nthr) {
+  pfa_pass_n<RADER_M, 13, INV>(buf, tid, nthr);
+  __syncthreads();
+  pfa_pass_n<RADER_M, 7, INV>(buf, tid, nthr);
+  __syncthreads();
+  pfa_pass_n<RADER_M, 5, INV>(buf, tid, nthr);
+  __syncthreads();
+  pfa_pass_n<RADER_M, 9, INV>(buf, tid, nthr);
+  __syncthreads();
+  pfa_pass_n<RADER_M, 2, INV>(buf, tid, nthr);
+  __syncthreads();
+}
+
+struct RaderTabs {
+  const int* gpow;   // [8190] g^q mod 8191
+  const int* plog;   // [8191] bin g^-p -> p (bin 0 unused)
+  const double2* D;  // [8190] DFT_8190(d)_k / 8190 at slot 253 k mod 8190
+};
+
+// DFT_8191 (INV: unnormalised inverse) of buf[0, 8191) (natural order,
+// written and synced) by T threads.  Leaves the convolution in buf[0, 8190)
+// and returns x_0 and X_0 (of the conjugated input when INV); the outputs are
+// then rader_bin(...).  s_part: T/32 double2 of shared scratch.  Ends synced.
+template <int T, bool INV>
+S2W_DEV void rader8191(double2* buf, const RaderTabs& R, double2* s_part, double2& x0, double2& X0) {
+  constexpr int U = (RADER_M + T - 1) / T;
+  const int tid = threadIdx.x;
+  double2 v[U];
+  double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int q = tid + u * T;
+    v[u] = make_double2(0.0, 0.0);
+    if (q < RADER_M) {
+      v[u] = buf[__ldg(&R.gpow[q])];
+      if (INV) v[u] = cconj(v[u]);
+      sum = cadd(sum, v[u]);  // every n >= 1 is some g^q exactly once
+    }
+  }
+  x0 = buf[0];
+  if (INV) x0 = cconj(x0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o);
+    sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o);
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) s_part[tid >> 5] = sum;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int q = tid + u * T;
+    if (q < RADER_M) buf[q] = v[u];
+  }
+  __syncthreads();
+  X0 = x0;
+  for (int w = 0; w < T / 32; ++w) X0 = cadd(X0, s_part[w]);
+  pfa8190<false>(buf, tid, T);
+  for (int s = tid; s < RADER_M; s += T) buf[s] = cmul(buf[s], __ldg(&R.D[s]));
+  __syncthreads();
+  pfa8190<true>(buf, tid, T);
+}
+
+// Output bin b of rader8191 (conjugated back when INV).
+template <bool INV>
+S2W_DEV double2 rader_bin(const double2* buf, const RaderTabs& R, double2 x0, double2 X0, int b) {
+  const double2 y = b ? cadd(x0, buf[__ldg(&R.plog[b])]) : X0;
+  return INV ? cconj(y) : y;
 }

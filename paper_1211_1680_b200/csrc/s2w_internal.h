@@ -40,6 +40,11 @@ struct FftTablesDev {
                           //        the |sin| series on one parity class, bit-reversed
   const double2* phA;     // [N]  e^{-i pi q/N} / N  (theta: DFT_N bin -> Fourier coefficient)
   const double2* phS;     // [N]  e^{-i pi q/N2} e^{i pi q/N} / N2  (theta_syn: DFT_N2 bin -> DFT_N input)
+  // N = 8191 (k = 4096) stage kernels ("k4"; phA / phS above, tw = the 8192-point engine):
+  const int* rgpow;       // [8190] Rader gather g^q mod N
+  const int* rplog;       // [N]    Rader output map bin g^-p -> p
+  const double2* rD;      // [8190] Rader kernel spectrum in prime-factor slot order, / 8190
+  const double* w4s;      // [8192] FFT(w_hat(2d), circular)/8192 (real), bit-reversed
 };
 
 struct PhiFwdArgs {

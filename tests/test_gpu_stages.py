@@ -101,12 +101,13 @@ def test_phi_stages_split_mode_vs_numpy(env, L, real):
     assert np.abs(got_f - np.swapaxes(F, 1, 2)).max() <= 1e-14 * np.abs(F).max() * np.log2(N)
 
 
+@pytest.mark.parametrize("L", [2048, 4096])
 @pytest.mark.parametrize("real", [True, False])
-def test_theta_stage_pfa_L2048_vs_oracle(env, real):
-    """L = 2048: the theta stage's DFT_4095 runs on the prime-factor engine."""
+def test_theta_stage_pfa_vs_oracle(env, real, L):
+    """L = 2048: the theta stage's DFT_4095 runs on the prime-factor engine;
+    L = 4096: DFT_8191 by Rader over the prime-factor DFT_8190 (k4 kernels)."""
     from oracle import oracle as orc
 
-    L = 2048
     rng = np.random.default_rng(11 + real)
     maps = rng.standard_normal((1, L, 2 * L - 1))
     if not real:
@@ -114,4 +115,8 @@ def test_theta_stage_pfa_L2048_vs_oracle(env, real):
     maps[:, -1, :] = maps[:, -1, :1]  # a sampled function is constant on the pole ring
     H = _run_forward(env, 1, L, maps if not real else maps.astype(complex), real, 1)
     Href = orc.mw_theta_stage_rings(orc.rings_forward(maps, L, real), L, real)
-    assert np.abs(H - Href).max() <= 1e-12 * np.abs(Href).max()
+    # at L = 4096 the oracle's dense double-precision operator (8191-term dot
+    # products) carries ~2e-12 itself: the Rader kernels and the former
+    # split-mode Bluestein kernels agree to 2.5e-15 and both sit 2.1e-12 from it
+    tol = 1e-12 if L <= 2048 else 4e-12
+    assert np.abs(H - Href).max() <= tol * np.abs(Href).max()
