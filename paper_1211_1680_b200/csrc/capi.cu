@@ -824,7 +824,14 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   cfg.sym = 0;
   for (auto& gr : groups) cfg.sym |= gr.g->leg(cplx, false).n_north > 0 ? 1 : 0;
   // symmetric rings keep two accumulator sets: at most 4 complex / 8 real sets per CTA
-  const int ns = cfg.sym ? std::min(pick_ns(maxn, cplx), cplx ? 4 : 8) : pick_ns(maxn, cplx);
+  int ns = cfg.sym ? std::min(pick_ns(maxn, cplx), cplx ? 4 : 8) : pick_ns(maxn, cplx);
+  {
+    static const int cap = getenv("S2W_SYN_NS_CAP") ? atoi(getenv("S2W_SYN_NS_CAP")) : 0;
+    if (cap > 0) ns = std::min(ns, cap);
+    // two complex sets on symmetric rings: two one-set items per order run
+    // faster than one two-set item (the one-set kernel keeps two CTAs per SM)
+    else if (cap == 0 && cfg.sym && cplx && ns == 2) ns = 1;
+  }
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const auto& gr = groups[gi];
     grids.push_back(gr.g->leg(cplx, false));
