@@ -203,3 +203,21 @@ def test_round_trip_L2048_pfa(sw, scheme, real):
     x = sht.synthesis(torch.from_numpy(f[None].copy()).cuda(), real=real)
     back = sht.analysis(x).cpu().numpy()[0]
     assert np.abs(back - f).max() <= 1e-10 * max(1.0, np.abs(f).max())
+
+
+@pytest.mark.parametrize("real", [False, True])
+def test_round_trip_L2048_batch2(sw, real):
+    """Two maps per call at L = 2048: the k2 stage kernels over several sets
+    (rows of set 1 follow set 0) and the batched Legendre kernels."""
+    import torch
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform
+
+    L = 2048
+    f = np.stack([sw.gaussian_coeffs(L, np.random.default_rng(40 + b), real_signal=real).coeffs
+                  for b in range(2)])
+    sht = SphericalHarmonicTransform(sw.SamplingScheme.MW, L)
+    x = sht.synthesis(torch.from_numpy(f).cuda(), real=real)
+    one = sht.synthesis(torch.from_numpy(f[1:].copy()).cuda(), real=real)
+    assert torch.equal(x[1:], one)  # set 1 does not depend on set 0
+    back = sht.analysis(x).cpu().numpy()
+    assert np.abs(back - f).max() <= 1e-10 * max(1.0, np.abs(f).max())
