@@ -736,25 +736,33 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
       dd[j] = cld(std::cos(ang), std::sin(ang));
       gi = gi * ginv % N;
     }
-    // DFT_8190 of d in long double (direct O(R log R) via the radix-2 long
-    // double FFT would need a power of two: use the exact O(R^2) sum, once per grid)
+    // DFT_8190 of d in long double by the same prime-factor passes as the
+    // kernels (pfa.cuh): natural order in, bin k at slot 253 k mod 8190 out,
+    // which is exactly the slot order the kernels multiply in
     std::vector<double2> Dslot(R);
     {
-      std::vector<cld> tw(R);
-      for (int t = 0; t < R; ++t) {
-        const ld ang = -2.0L * PI_L * (ld)t / (ld)R;
-        tw[t] = cld(std::cos(ang), std::sin(ang));
-      }
-      for (int kk = 0; kk < R; ++kk) {
-        cld acc(0, 0);
-        long long idx = 0;
-        for (int j = 0; j < R; ++j) {
-          acc += dd[j] * tw[idx];
-          idx += kk;
-          if (idx >= R) idx -= R;
+      std::vector<cld> b(dd);
+      for (int P : {13, 7, 5, 9, 2}) {
+        const int A = R / P;
+        std::vector<cld> W(P * P);
+        for (int u = 0; u < P; ++u)
+          for (int v = 0; v < P; ++v) {
+            const ld ang = -2.0L * PI_L * (ld)((u * v) % P) / (ld)P;
+            W[u * P + v] = cld(std::cos(ang), std::sin(ang));
+          }
+        std::vector<cld> x(P), y(P);
+        for (int r = 0; r < A; ++r) {
+          for (int j = 0; j < P; ++j) x[j] = b[(P * r + j * A) % R];
+          for (int u = 0; u < P; ++u) {
+            cld acc(0, 0);
+            for (int v = 0; v < P; ++v) acc += W[u * P + v] * x[v];
+            y[u] = acc;
+          }
+          for (int j = 0; j < P; ++j) b[(P * r + j * A) % R] = y[j];
         }
-        Dslot[(long long)kk * STEP % R] = d2(acc / (ld)R);
       }
+      for (int i = 0; i < R; ++i) Dslot[i] = d2(b[i] / (ld)R);
+      (void)STEP;
     }
     std::vector<cld> w4(M4, cld(0, 0));
     for (int d = -(M4 / 2 - 1); d <= M4 / 2 - 1; ++d)
