@@ -185,10 +185,41 @@ def config_cases():
     np.savez_compressed(OUT / "configs.npz", **d)
 
 
+def config_wavelet_cases():
+    """Wavelet scale maps at the full C2 (L=256, real, lambda=2, J0=2) and C3
+    (L=1024, complex, lambda=2, J0=3) sizes, multires, MW, map 0 of each batch.
+    As in wavelet_cases the reference cannot analyse MW maps, so its scale maps
+    are its own harmonic tiling of the seeded f_lm (transform.py:129-150)
+    followed by its own MW synthesis on each scale grid (transform.py:108-114,
+    212-229).  Stored as seeded subsamples + norms, like config_cases."""
+    d = {}
+    specs = {
+        "C2": (256, 2.0, 2, True, lambda l: np.where(l >= 2, 1.0 / np.maximum(l * (l + 1), 1), 0.0)),
+        "C3": (1024, 2.0, 3, False, flat),
+    }
+    for name, (L, lam, j0, real, spec) in specs.items():
+        f = scaled_coeffs(L, 1000, real, spec)
+        cfg = sw.TransformConfig(L, lam, j0, scheme=MW, multires=True)
+        kern = sw.kernels_for(cfg)
+        wc = sw.wav_analysis_harmonic(f, kern, truncate=True)
+        grids = sw.transform._scale_grids(cfg, kern)
+        d[f"{name}_bands"] = np.array([g.L for g in grids])
+        for j, (s, g) in enumerate(zip([wc.scaling, *wc.wavelets], grids)):
+            m = sw.sh_synthesis(s, g).values
+            idx, vals = sub(m, 4096, 50 + j)
+            d[f"{name}_s{j}_idx"] = idx
+            d[f"{name}_s{j}_vals"] = vals
+            d[f"{name}_s{j}_norm2"] = np.array([np.sum(np.abs(m) ** 2)])
+            d[f"{name}_s{j}_max"] = np.array([np.abs(m).max()])
+    np.savez_compressed(OUT / "configs_wav.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs", "denoise", "mapio"]
+    which = sys.argv[1:] or ["sht", "legendre", "kernels", "wavelet", "configs", "configs_wav",
+                             "denoise", "mapio"]
     for w in which:
         {"sht": sht_cases, "legendre": legendre_cases, "kernels": kernel_cases,
-         "wavelet": wavelet_cases, "configs": config_cases, "denoise": denoise_cases,
+         "wavelet": wavelet_cases, "configs": config_cases,
+         "configs_wav": config_wavelet_cases, "denoise": denoise_cases,
          "mapio": mapio_cases}[w]()
         print("wrote", w)

@@ -136,3 +136,63 @@ def test_oracle_wavelets_match_reference(golden, name, scheme):
     rec = orc.wav_synthesis_pixel(maps, L, real, scheme, kern.table(), bands)
     back = orc.sh_analysis(rec, L, real, scheme)[0]
     assert np.abs(back - f).max() <= 1e-10
+
+
+@pytest.mark.parametrize("L,lam,j0,multires", [(64, 2.0, 0, False), (256, 2.0, 2, True),
+                                               (1024, 2.0, 3, True), (2048, 3.0, 2, True),
+                                               (4096, 2.0, 0, True), (128, 3.0, 2, True)])
+def test_oracle_bands_match_kernel_tables(golden, L, lam, j0, multires):
+    """The oracle's own band layout (reference tiling.py:58-73, 304-309) equals
+    the reference's (kernels.npz) and the product's host tables."""
+    from paper_1211_1680_b200.tiling import KernelFamily, TilingParams, build_kernels
+
+    k = build_kernels(TilingParams(L, lam, j0), KernelFamily.SCALE_DISCRETISED)
+    want = [k.scaling_bandlimit, *k.scale_bandlimits] if multires else [L] * (len(k.psi) + 1)
+    assert orc.sd_bands(L, lam, j0, multires) == want
+    tag = f"SCALE_DISCRETISED_{L}_{lam:g}_{j0}"
+    g = golden("kernels")
+    if multires and f"bands_{tag}" in g:
+        assert orc.sd_bands(L, lam, j0, True) == list(g[f"bands_{tag}"])
+
+
+def test_oracle_c2_scale_maps_match_reference(golden):
+    """C2 at full size (L = 256, real, lambda = 2, J0 = 2, multires): the oracle's
+    scale maps of the seeded map 0 vs the reference's (configs_wav.npz)."""
+    import bench
+    from paper_1211_1680_b200.tiling import KernelFamily, TilingParams, build_kernels
+
+    g = golden("configs_wav")
+    L = 256
+    f = bench.seeded_coeffs(L, True, "cl", 1000)
+    kern = build_kernels(TilingParams(L, 2.0, 2), KernelFamily.SCALE_DISCRETISED)
+    bands = orc.sd_bands(L, 2.0, 2, True)
+    assert bands == list(g["C2_bands"])
+    smap = orc.sh_synthesis(f[None], L, True, "mw")
+    maps = orc.wav_analysis_pixel(smap, L, True, "mw", kern.table(), bands)
+    for j, m in enumerate(maps):
+        v = m[0].reshape(-1)
+        assert rel_err(v[g[f"C2_s{j}_idx"]], g[f"C2_s{j}_vals"]) <= 1e-10, j
+
+
+def test_oracle_polar_rings_l4096_vs_mpmath():
+    """The checker's long-double recursion on the first MW rings of L = 4096,
+    where the double (reference) arithmetic drifts by ~1.6e-10 of the P_l
+    scale (the recursion's own rounding near x = 1), vs mpmath at 40 digits."""
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.dps = 40
+    L = 4096
+    N = 2 * L - 1
+    worst_precise, worst_double = 0.0, 0.0
+    for t in (0, 1, 3):
+        theta = (2 * t + 1) * math.pi / N
+        tab = orc.legendre_table(L, theta)
+        tabd = orc.legendre_table(L, theta, precise=False)
+        x = mpmath.cos(mpmath.mpf(theta))
+        for ell, m in ((4095, 0), (4000, 0), (4095, 1), (2000, 0), (4095, 5)):
+            p = mpmath.legenp(ell, m, x, type=2) * mpmath.sqrt(
+                (2 * ell + 1) / (4 * mpmath.pi) * mpmath.factorial(ell - m) / mpmath.factorial(ell + m))
+            scale = math.sqrt((2 * ell + 1) / (4 * math.pi))
+            worst_precise = max(worst_precise, abs(tab[ell, m] - float(p)) / scale)
+            worst_double = max(worst_double, abs(tabd[ell, m] - float(p)) / scale)
+    assert worst_precise <= 1e-12
+    assert worst_double > 1e-11  # the drift the checker exists to avoid
