@@ -7,8 +7,12 @@ One step = one wavelet analysis + synthesis round trip of the map.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
-N > 1 runs under torchrun, one replica per rank (each rank transforms its own
-seeded map; "scaling": "weak"); timing is the max over ranks of CUDA-event time.
+N > 1 runs under torchrun and, by default, partitions the ONE map of the
+config over the ranks as BASELINE C4/C5 name it (--mode shard: orders m for
+the Legendre/theta stages, theta rings for the phi stages, NCCL all-to-all
+between them; small scale bands placed whole on one rank; "scaling":
+"strong").  --mode replica runs one independent map per rank ("weak").
+Timing is the max over ranks of CUDA-event time.
 --impl reference times the CPU oracle port of the same path (oracle/, C with
 OpenMP, the reference itself being pure Python that cannot leave this repo's
 build container) on rank 0 only.

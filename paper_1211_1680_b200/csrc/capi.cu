@@ -13,6 +13,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -439,6 +440,22 @@ struct GridRes {
     return g;
   }
   int n_bins(bool cplx) const { return cplx ? N : k; }
+  // Free every device table (a half-built grid on a setup failure).  GL
+  // grids alias ana to syn.
+  void release() {
+    auto fr = [](auto*& p) {
+      if (p) cudaFree((void*)p);
+      p = nullptr;
+    };
+    const bool alias = ana.cos_t == syn.cos_t;
+    for (RingSet* rs : {&syn, &ana}) {
+      if (rs == &ana && alias) break;
+      fr(rs->cos_t), fr(rs->omc_t), fr(rs->sin_t), fr(rs->ring_w), fr(rs->act);
+    }
+    fr(tw), fr(octM), fr(chirp), fr(bl_fwd), fr(bl_inv), fr(ph1), fr(ph2), fr(wconv), fr(chirp2);
+    fr(bl_ev), fr(bl_fwd2), fr(ph4), fr(ph2d), fr(ph4d), fr(tw12), fr(phA), fr(phS), fr(rD);
+    fr(w2s), fr(w4s), fr(rgpow), fr(rplog), fr(pairs_r), fr(pairs_c), fr(pole_resp);
+  }
   // rough cost of the Legendre work for order m (ring-steps)
   double cost(int m, bool analysis) const {
     const RingSet& rs = (analysis || syn_on_ana()) ? ana : syn;
@@ -449,11 +466,16 @@ struct GridRes {
 };
 
 static std::map<std::tuple<int, int, int>, GridRes*> g_grids;
+// Private non-blocking stream for grid setup (uploads, probe and pole-response
+// launches), created and destroyed by get_grid under g_mu: setup never orders
+// against, or stalls, the caller's streams through the legacy stream 0.
+static cudaStream_t g_setup = nullptr;
 
 template <class T>
 static int upload_new(T** dst, const std::vector<T>& v) {
   CU(cudaMalloc(dst, std::max<size_t>(16, v.size() * sizeof(T))));
-  if (!v.empty()) CU(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  if (!v.empty())
+    CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g_setup));
   return S2W_OK;
 }
 
@@ -501,9 +523,10 @@ static int ring_set(RingSet& rs, const std::vector<double>& theta, const std::ve
   CHECK(upload_new(&rs.ring_w, w));
   int* d_mmax = nullptr;
   CU(cudaMalloc(&d_mmax, sizeof(int) * n));
-  CU(launch_leg_probe(k, n, rs.cos_t, rs.sin_t, seed_c, d_mmax, 0));
+  CU(launch_leg_probe(k, n, rs.cos_t, rs.sin_t, seed_c, d_mmax, g_setup));
   std::vector<int> mmax(n);
-  CU(cudaMemcpy(mmax.data(), d_mmax, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(mmax.data(), d_mmax, sizeof(int) * n, cudaMemcpyDeviceToHost, g_setup));
+  CU(cudaStreamSynchronize(g_setup));
   cudaFree(d_mmax);
   rs.act_host.assign(k, make_int2(0, 0));
   for (int m = 0; m < k; ++m) {
@@ -548,13 +571,15 @@ static int theta_setup(GridRes* g) {
   ta.in = d_imp;
   ta.out = g->pole_resp;
   ta.scratch = scratch;
-  CU(launch_theta(ta, 0));
-  CU(cudaStreamSynchronize(0));
+  CU(launch_theta(ta, g_setup));
+  CU(cudaStreamSynchronize(g_setup));
   cudaFree(d_imp);
   cudaFree(one);
   if (scratch) cudaFree(scratch);
   return S2W_OK;
 }
+
+static int build_grid(GridRes* g, int dev, int scheme, int k);
 
 static int get_grid(int dev, int scheme, int k, GridRes** out) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -565,9 +590,23 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     return S2W_OK;
   }
   if (k < 1 || k > S2W_MAX_L) return fail(S2W_EPARAM, "band-limit %d out of range [1, %d]", k, S2W_MAX_L);
+  CU(cudaStreamCreateWithFlags(&g_setup, cudaStreamNonBlocking));
+  std::unique_ptr<GridRes> g(new GridRes());
+  int r = build_grid(g.get(), dev, scheme, k);
+  if (r == S2W_OK) r = cudaStreamSynchronize(g_setup) == cudaSuccess ? S2W_OK : fail(S2W_ECUDA, "grid setup");
+  cudaStreamDestroy(g_setup);
+  g_setup = nullptr;
+  if (r != S2W_OK) {
+    g->release();  // no half-built grid leaks its tables
+    return r;
+  }
+  *out = g_grids[key] = g.release();
+  return S2W_OK;
+}
+
+static int build_grid(GridRes* g, int dev, int scheme, int k) {
   DeviceTables* dt;
   CHECK(device_tables(dev, &dt));
-  GridRes* g = new GridRes();
   g->device = dev;
   g->scheme = scheme;
   g->k = k;
@@ -785,8 +824,6 @@ static int get_grid(int dev, int scheme, int k, GridRes** out) {
     CHECK(upload_new(&g->phS, phS));
   }
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
-  g_grids[key] = g;
-  *out = g;
   return S2W_OK;
 }
 
@@ -1274,16 +1311,23 @@ struct s2w_wav_plan {
     }
     CU(cudaEventRecord(fork, st));
     const int ns = std::min<int>(NSIDE, (int)order.size());
-    for (int i = 0; i < ns; ++i) CU(cudaStreamWaitEvent(side[i], fork, 0));
-    for (size_t i = 0; i < order.size(); ++i) {
+    int r = S2W_OK, forked = 0;
+    for (; forked < ns && r == S2W_OK; ++forked)
+      if (cudaStreamWaitEvent(side[forked], fork, 0) != cudaSuccess)
+        r = fail(S2W_ECUDA, "side stream fork failed");
+    for (size_t i = 0; i < order.size() && r == S2W_OK; ++i) {
       const int j = order[i], q = (int)(i % NSIDE);
-      CHECK(f(j, side[q], sscratch[q].as<double2>(), Grj[j] ? Grj[j]->as<double2>() : nullptr));
+      r = f(j, side[q], sscratch[q].as<double2>(), Grj[j] ? Grj[j]->as<double2>() : nullptr);
     }
-    for (int i = 0; i < ns; ++i) {
-      CU(cudaEventRecord(join[i], side[i]));
-      CU(cudaStreamWaitEvent(st, join[i], 0));
+    // join every forked side stream on every exit path: a capture must end
+    // with all branches joined, and eager callers must stay ordered after
+    // side work that reuses sscratch
+    for (int i = 0; i < forked; ++i) {
+      const bool ok = cudaEventRecord(join[i], side[i]) == cudaSuccess &&
+                      cudaStreamWaitEvent(st, join[i], 0) == cudaSuccess;
+      if (!ok && r == S2W_OK) r = fail(S2W_ECUDA, "side stream join failed");
     }
-    return S2W_OK;
+    return r;
   }
 };
 

@@ -26,6 +26,22 @@ def _on_device(t):
     return t.to(device=f"cuda:{_device.device_index()}", non_blocking=True)
 
 
+def _checked(t, shape, dtype, what):
+    """The C ABI trusts its pointers: refuse anything whose extent, element
+    type, device or layout differs from what the kernels will address."""
+    th = _device.torch()
+    if not isinstance(t, th.Tensor):
+        raise ParameterError(f"{what}: expected a torch tensor, got {type(t).__name__}")
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+        raise ParameterError(f"{what}: expected {dtype} of shape {tuple(shape)}, "
+                             f"got {t.dtype} of shape {tuple(t.shape)}")
+    if not t.is_cuda or t.device.index != _device.device_index():
+        raise ParameterError(f"{what}: must live on cuda:{_device.device_index()}, got {t.device}")
+    if not t.is_contiguous():
+        raise ParameterError(f"{what}: must be contiguous")
+    return t
+
+
 class SphericalHarmonicTransform:
     """SHT on one grid for batches of device tensors."""
 
@@ -37,8 +53,14 @@ class SphericalHarmonicTransform:
     def synthesis(self, flm, real: bool = False):
         th = _device.torch()
         flm = _on_device(flm)
+        if flm.dim() != 2 or flm.shape[0] < 1:
+            raise ParameterError(f"flm: expected (batch, Lc*Lc), got shape {tuple(flm.shape)}")
         n = flm.shape[0]
         Lc = int(round(np.sqrt(flm.shape[1])))
+        if Lc * Lc != flm.shape[1] or not 1 <= Lc <= self.grid.L:
+            raise ParameterError(f"flm: {flm.shape[1]} coefficients is not Lc*Lc with "
+                                 f"1 <= Lc <= {self.grid.L}")
+        _checked(flm, (n, Lc * Lc), th.complex128, "flm")
         g = self.grid
         dt = th.float64 if real else th.complex128
         out = th.empty((n, g.n_theta, g.n_phi), dtype=dt, device=flm.device)
@@ -51,8 +73,12 @@ class SphericalHarmonicTransform:
         th = _device.torch()
         maps = _on_device(maps)
         real = not maps.is_complex()
+        if maps.dim() != 3 or maps.shape[0] < 1:
+            raise ParameterError(f"maps: expected (batch, n_theta, n_phi), got {tuple(maps.shape)}")
         n = maps.shape[0]
-        L = self.grid.L
+        g = self.grid
+        _checked(maps, (n, g.n_theta, g.n_phi), th.float64 if real else th.complex128, "maps")
+        L = g.L
         out = th.empty((n, L * L), dtype=th.complex128, device=maps.device)
         _native.check(_native.load().s2w_sh_analysis(
             self.plan.handle, n, int(real), _device.ptr(maps), _device.ptr(out),
@@ -84,6 +110,13 @@ class WaveletTransform:
         the caller's stream (per-stage profiling); results are identical."""
         _native.check(_native.load().s2w_wav_plan_set_concurrency(self.plan.handle, int(bool(on))))
 
+    def _check_scale_maps(self, maps, what):
+        if len(maps) != len(self.grids):
+            raise ParameterError(f"{what}: expected {len(self.grids)} scale maps "
+                                 f"(scaling + wavelets), got {len(maps)}")
+        for j, (m, g) in enumerate(zip(maps, self.grids)):
+            _checked(m, (self.batch, g.n_theta, g.n_phi), self._dtype(), f"{what}[{j}]")
+
     def alloc_scale_maps(self):
         th = _device.torch()
         return [th.empty((self.batch, g.n_theta, g.n_phi), dtype=self._dtype(),
@@ -91,10 +124,9 @@ class WaveletTransform:
 
     def analysis(self, x, outs=None):
         """x: (batch, L, 2L-1) map tensor -> [scaling, j0..J] map tensors."""
-        x = _on_device(x)
-        if tuple(x.shape) != self.map_shape or x.dtype != self._dtype():
-            raise ParameterError(f"expected {self._dtype()} tensor of shape {self.map_shape}")
-        outs = self.alloc_scale_maps() if outs is None else outs
+        x = _checked(_on_device(x), self.map_shape, self._dtype(), "x")
+        outs = self.alloc_scale_maps() if outs is None else list(outs)
+        self._check_scale_maps(outs, "outs")
         _native.check(_native.load().s2w_wav_analysis_pixel(
             self.plan.handle, _device.ptr(x), _device.ptr_array(outs), _device.stream_handle()))
         return outs
@@ -102,8 +134,10 @@ class WaveletTransform:
     def synthesis(self, maps, out=None):
         th = _device.torch()
         maps = [_on_device(m) for m in maps]
+        self._check_scale_maps(maps, "maps")
         if out is None:
             out = th.empty(self.map_shape, dtype=self._dtype(), device=maps[0].device)
+        _checked(out, self.map_shape, self._dtype(), "out")
         _native.check(_native.load().s2w_wav_synthesis_pixel(
             self.plan.handle, _device.ptr_array(maps), _device.ptr(out), _device.stream_handle()))
         return out
@@ -200,6 +234,9 @@ class WaveletTransform:
                 out_free[b].record(d2h)
         comp.wait_stream(d2h)
         comp.wait_stream(h2d)
+        # host outputs are complete when this returns, like the synchronous
+        # outputs[i].copy_(round_trip(inputs[i])) it stands for
+        d2h.synchronize()
         return outputs
 
     def flm(self):

@@ -84,7 +84,8 @@ def test_theta_stage_vs_oracle(env, L, real):
 
 @pytest.mark.parametrize("L", [2049, 4096])
 @pytest.mark.parametrize("real", [True, False])
-def test_phi_stages_split_mode_vs_numpy(env, L, real):
+def test_phi_stages_large_odd_n_vs_numpy(env, L, real):
+    """L = 2049: generic split-mode Bluestein rows; L = 4096: the k4 Rader kernels."""
     rng = np.random.default_rng(L)
     N = 2 * L - 1
     nb = L if real else N
