@@ -308,17 +308,45 @@ static std::vector<double2> octant_table(int logM) {
 }
 
 // ------------------------------------------------------------------ per-device seed table
-static const int SEED_KMAX = 16384;
+static const int SEED_KMAX = S2W_SEED_KMAX;
 // Largest band limit: ring DFTs of N = 2L-1 need a Bluestein convolution of
 // 2^ceil(log2(4L-3)) <= 2^14 points (split mode).
 static const int S2W_MAX_L = 4096;
+static_assert(S2W_MAX_L + 32 <= S2W_REIN_STRIDE, "Reinsch rows cover every chunk of the largest band");
 
 struct DeviceTables {
-  double* seed_c = nullptr;  // c_m, m < SEED_KMAX
+  double* seed_c = nullptr;  // c_m, m < SEED_KMAX, then the Reinsch table (rein_table)
 };
 
 static std::mutex g_mu;
 static std::map<int, DeviceTables> g_dev;
+
+// Reinsch form of the low orders' recursion (legendre_kernels.cu,
+// ring_step_rein).  With a_l, b_l of sht.py:146-152 (exact, long double) and
+// rho_l the ratio P_l / P_{l-1} of the recursion's solution at x = 1
+// (rho_{m+1} = a_{m+1}, rho_l = a_l - b_l / rho_{l-1}):
+//   lambda'_l = rho_l / a_l,  kappa'_l = b_l / (a_l rho_{l-1}),
+// and the seed degree l = m gets (0, 1).  These are the ratios of the
+// normalised state Q_l = P_l / gamma_l whatever the chunking, since gamma
+// only rescales both state values by a common factor.
+static void rein_rows(std::vector<double2>& tab) {
+  tab.assign((size_t)S2W_REIN_M * S2W_REIN_STRIDE, make_double2(1.0, 0.0));
+  for (int m = 0; m < S2W_REIN_M; ++m) {
+    double2* row = tab.data() + (size_t)m * S2W_REIN_STRIDE;
+    row[m] = make_double2(0.0, 1.0);
+    ld rho_prev = 0.0L;
+    for (int l = m + 1; l < S2W_REIN_STRIDE; ++l) {
+      const ld L_ = l, M_ = m, den = L_ * L_ - M_ * M_;
+      const ld a = std::sqrt((4.0L * L_ * L_ - 1.0L) / den);
+      const ld b = std::sqrt((2.0L * L_ + 1.0L) / (2.0L * L_ - 3.0L) *
+                             ((L_ - 1.0L) * (L_ - 1.0L) - M_ * M_) / den);
+      const ld rho = (l == m + 1) ? a : a - b / rho_prev;
+      const ld kap = (l == m + 1) ? 0.0L : b / (a * rho_prev);
+      row[l] = make_double2((double)(rho / a), (double)kap);
+      rho_prev = rho;
+    }
+  }
+}
 
 static int device_tables(int dev, DeviceTables** out) {
   auto it = g_dev.find(dev);
@@ -333,9 +361,13 @@ static int device_tables(int dev, DeviceTables** out) {
     v *= std::sqrt((ld)(2 * m + 1) / (ld)(2 * m));
     c[m] = (double)v;
   }
+  std::vector<double2> rein;
+  rein_rows(rein);
   DeviceTables t;
-  CU(cudaMalloc(&t.seed_c, sizeof(double) * SEED_KMAX));
-  CU(cudaMemcpy(t.seed_c, c.data(), sizeof(double) * SEED_KMAX, cudaMemcpyHostToDevice));
+  const size_t cb = sizeof(double) * SEED_KMAX, rb = sizeof(double2) * rein.size();
+  CU(cudaMalloc(&t.seed_c, cb + rb));
+  CU(cudaMemcpy(t.seed_c, c.data(), cb, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(t.seed_c + SEED_KMAX, rein.data(), rb, cudaMemcpyHostToDevice));
   g_dev[dev] = t;
   *out = &g_dev[dev];
   return S2W_OK;
@@ -835,8 +867,70 @@ static int pick_ns(int n, bool cplx) {
   return ns;
 }
 
+// Side stream for the Reinsch launch of the low orders (legendre_kernels.cu,
+// REIN): forked from and joined back into the caller's stream with events,
+// so it runs beside the plain launch (and CUDA-graph capture follows it).
+struct SideLane {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SideLane() = default;
+  SideLane(const SideLane&) = delete;
+  SideLane& operator=(const SideLane&) = delete;
+  ~SideLane() {
+    if (s) cudaStreamDestroy(s);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
+  int ensure() {
+    if (s) return S2W_OK;
+    // highest priority: the low orders are the heaviest items, so their CTAs
+    // should take SMs before the plain launch's
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+    CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    return S2W_OK;
+  }
+  // launch `side_fn` on the lane and `main_fn` on st, joined back into st on
+  // every exit path
+  template <class F, class G>
+  int fork_join(cudaStream_t st, F&& side_fn, G&& main_fn) {
+    CHECK(ensure());
+    CU(cudaEventRecord(fork, st));
+    CU(cudaStreamWaitEvent(s, fork, 0));
+    const cudaError_t e1 = side_fn(s);
+    const cudaError_t e2 = e1 == cudaSuccess ? main_fn(st) : cudaSuccess;
+    CU(cudaEventRecord(join, s));
+    CU(cudaStreamWaitEvent(st, join, 0));
+    CU(e1);
+    CU(e2);
+    return S2W_OK;
+  }
+};
+
+static int item_grid(const SynthItem& it) { return it.grid; }
+static int item_grid(const AnaItem&) { return 0; }  // analysis grids are all symmetric when sym
+
+// Items of the low orders on equator-symmetric ring sets go first (Reinsch
+// launch; the symmetric kernels sweep only their northern rings, x >= 0, where
+// the Reinsch form applies); returns their count.  Cost order is kept within
+// each part.  Asymmetric grids of a symmetric launch keep the plain recursion.
+template <class It>
+static int rein_partition(std::vector<It>& items, bool sym, const std::vector<LegGridDev>& grids,
+                          bool per_item_grid) {
+  if (!sym) return 0;
+  auto mid = std::stable_partition(items.begin(), items.end(), [&](const It& i) {
+    if (i.it.m >= S2W_REIN_M) return false;
+    return !per_item_grid || grids[item_grid(i.it)].n_north > 0;
+  });
+  return (int)(mid - items.begin());
+}
+
 struct SynthCfg {
   bool built = false;
+  int n_rein = 0;
+  mutable SideLane lane;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, items;
   int n_items = 0, ns = 1, cplx = 1, win = 32, sym = 0;
@@ -844,6 +938,8 @@ struct SynthCfg {
 
 struct AnaCfg {
   bool built = false;
+  int n_rein = 0;
+  mutable SideLane lane;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, segs, items;
   int n_items = 0, ns = 1, cplx = 1, win = 32, sym = 0;
@@ -892,6 +988,7 @@ static int build_synth(SynthCfg& cfg, const std::vector<SynthGroupSpec>& groups,
   }
   std::stable_sort(items.begin(), items.end(),
                    [](const It& a, const It& b) { return a.cost > b.cost; });
+  cfg.n_rein = rein_partition(items, cfg.sym != 0, grids, true);
   std::vector<SynthItem> its;
   for (auto& i : items) its.push_back(i.it);
   CHECK(cfg.grids.upload(grids));
@@ -987,6 +1084,7 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   }
   std::stable_sort(items.begin(), items.end(),
                    [](const It& a, const It& b) { return a.cost > b.cost; });
+  cfg.n_rein = rein_partition(items, cfg.sym != 0, grids, false);
   std::vector<AnaItem> its;
   for (auto& i : items) its.push_back(i.it);
   CHECK(cfg.grids.upload(grids));
@@ -1013,10 +1111,21 @@ static int run_synth(const SynthCfg& cfg, const double* seed_c, double2* const* 
   a.ns = cfg.ns;
   a.win = cfg.win;
   a.sym = cfg.sym;
+  a.rein = 0;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_SYNTH, st);
-  CU(launch_leg_synth(a, st));
-  return S2W_OK;
+  if (cfg.n_rein == 0) {
+    CU(launch_leg_synth(a, st));
+    return S2W_OK;
+  }
+  LegSynthArgs r = a;
+  r.n_items = cfg.n_rein;
+  r.rein = 1;
+  a.items += cfg.n_rein;
+  a.n_items -= cfg.n_rein;
+  ++g_launches;
+  return cfg.lane.fork_join(st, [&](cudaStream_t s) { return launch_leg_synth(r, s); },
+                            [&](cudaStream_t s) { return launch_leg_synth(a, s); });
 }
 
 static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs,
@@ -1032,10 +1141,21 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
   a.ns = cfg.ns;
   a.win = cfg.win;
   a.sym = cfg.sym;
+  a.rein = 0;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_ANA, st);
-  CU(launch_leg_ana(a, st));
-  return S2W_OK;
+  if (cfg.n_rein == 0) {
+    CU(launch_leg_ana(a, st));
+    return S2W_OK;
+  }
+  LegAnaArgs r = a;
+  r.n_items = cfg.n_rein;
+  r.rein = 1;
+  a.items += cfg.n_rein;
+  a.n_items -= cfg.n_rein;
+  ++g_launches;
+  return cfg.lane.fork_join(st, [&](cudaStream_t s) { return launch_leg_ana(r, s); },
+                            [&](cudaStream_t s) { return launch_leg_ana(a, s); });
 }
 
 // ------------------------------------------------------------------ shared pipeline steps

@@ -164,16 +164,30 @@ struct AnaItem {
   int m, seg0, nseg;
 };
 
+// The seed table c_m (LegSynthArgs/LegAnaArgs::seed_c) has S2W_SEED_KMAX
+// entries and is followed, in the same allocation, by the Reinsch table of
+// the low orders: for m < S2W_REIN_M, rein[m * S2W_REIN_STRIDE + l] =
+// (lambda'_l, kappa'_l), the x = 1 solution ratios of the normalised
+// recursion computed in long double on the host (legendre_kernels.cu,
+// ring_step_rein).  The table depends on (l, m) only, not on the rings.
+constexpr int S2W_SEED_KMAX = 16384;
+constexpr int S2W_REIN_M = 32;
+constexpr int S2W_REIN_STRIDE = 4096 + 64;
+__host__ __device__ inline const double2* rein_table(const double* seed_c) {
+  return reinterpret_cast<const double2*>(seed_c + S2W_SEED_KMAX);
+}
+
 struct LegSynthArgs {
   const LegGridDev* grids;
   const SynthSet* sets;
   const SynthItem* items;
-  const double* seed_c;  // [kmax] c_m
+  const double* seed_c;  // [S2W_SEED_KMAX] c_m, then the Reinsch table (rein_table)
   int n_items;
   int cplx;
   int ns;  // compile-time set width selected by the launcher
   int win; // degrees per shared-memory window (leg_synth_window)
   int sym; // every grid is equator-symmetric (LegGridDev::n_north > 0)
+  int rein; // the items are orders m < S2W_REIN_M (Reinsch recursion; sym only)
   double2* bufs[S2W_NBUF];
 };
 
@@ -188,6 +202,7 @@ struct LegAnaArgs {
   int ns;
   int win;  // degrees per window (leg_ana_window)
   int sym;  // every grid is equator-symmetric (LegGridDev::n_north > 0)
+  int rein; // the items are orders m < S2W_REIN_M (Reinsch recursion; sym only)
   double2* bufs[S2W_NBUF];
 };
 

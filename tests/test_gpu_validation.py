@@ -37,9 +37,11 @@ def test_sht_rejects_bad_tensors(env):
         sht.analysis(th.zeros((2, L, 2 * L), dtype=th.complex128, device=dev))
     with pytest.raises(sw.ParameterError):
         sht.analysis(th.zeros((2, L + 1, 2 * L - 1), dtype=th.float64, device=dev))
-    with pytest.raises(sw.ParameterError):   # non-contiguous view of the right shape
-        big = th.zeros((2, L, 2 * (2 * L - 1)), dtype=th.complex128, device=dev)
-        sht.analysis(big[:, :, ::2])
+    # a non-contiguous input view is copied, not misread
+    big = th.zeros((2, L, 2 * (2 * L - 1)), dtype=th.float64, device=dev)
+    big[:, :, ::2] = 1.0
+    a = sht.analysis(big[:, :, ::2])
+    assert th.equal(a, sht.analysis(th.ones((2, L, 2 * L - 1), dtype=th.float64, device=dev)))
     assert float(sht.analysis(m).abs().max()) == 0.0
 
 
@@ -60,6 +62,9 @@ def test_wavelet_rejects_bad_scale_lists(env):
         wt.analysis(x.real.contiguous())
     with pytest.raises(sw.ParameterError):
         wt.round_trip(x, out=th.zeros((1, L, 2 * L - 1), dtype=th.float64, device="cuda"))
+    with pytest.raises(sw.ParameterError):   # outputs must be contiguous (written in place)
+        wide = th.zeros((1, L, 2 * (2 * L - 1)), dtype=th.complex128, device="cuda")
+        wt.round_trip(x, out=wide[:, :, ::2])
     rec = wt.synthesis(outs)
     th.cuda.synchronize()
     assert float(rec.abs().max()) == 0.0
