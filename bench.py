@@ -120,16 +120,18 @@ def stage_bytes(cfg, bands):
 
 
 def stage_flops(cfg, bands):
-    """Canonical FLOPs per launch of the two grouped Legendre launches of each direction."""
+    """Canonical FLOPs per round trip of each Legendre stage.  Analysis
+    direction: leg_ana at L, leg_synth over the scale grids; synthesis: the
+    mirror.  Divided by the stage's measured time per round trip (not per
+    launch: the launch count depends on the path -- grouped, per scale when
+    sharded, plus the Reinsch launch of the low orders)."""
     L, B, real = cfg["L"], cfg["batch"], cfg["real"]
     groups = {}
     for k in bands:
         groups[k] = groups.get(k, 0) + B
     grouped = sum(legendre_flops(k, n, real) for k, n in groups.items())
     top = legendre_flops(L, B, real)
-    # analysis direction: leg_ana = top, leg_synth = grouped; synthesis: the mirror
-    return {"leg_ana": (top + grouped) / 2.0, "leg_synth": (top + grouped) / 2.0,
-            "per_rt": 2.0 * (top + grouped)}
+    return {"leg_ana": top + grouped, "leg_synth": top + grouped, "per_rt": 2.0 * (top + grouped)}
 
 
 class ClockSampler:
@@ -195,6 +197,9 @@ def run_ours(args, cfgname):
     from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
 
     ws, rank, local = dist_env()
+    # NCCL's banner / warnings go to stderr: stdout carries the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     torch.cuda.set_device(local)
     mode = args.mode or ("shard" if ws > 1 else "single")
     if ws > 1 or mode == "shard":
@@ -316,8 +321,8 @@ def run_ours(args, cfgname):
 
     def e2e_steps(k):
         if mode == "shard":
-            for _ in range(k):
-                out_host[0].copy_(step(x_host.cuda(non_blocking=True)), non_blocking=True)
+            for i in range(k):
+                out_host[i & 1].copy_(step(x_host.cuda(non_blocking=True)), non_blocking=True)
         else:
             wt.round_trip_stream([x_host] * k, [out_host[i & 1] for i in range(k)])
 
@@ -341,6 +346,13 @@ def run_ours(args, cfgname):
     e2e = maps_per_step * args.steps / (ms_e2e / 1e3)
     nbytes = x.numel() * x.element_size()
 
+    # --- end to end through the numpy drop-in, as the reference's run_trial
+    # times it (bench.py:84-92): host SphereMap(s) -> wav_analysis_pixel ->
+    # host WaveletDecomposition(s) -> wav_synthesis_pixel -> host SphereMap(s);
+    # every scale map crosses PCIe in both directions, synchronously
+    dropin = None
+    if mode != "shard":
+        dropin = dropin_e2e(sw, tcfg, x, real, args, barrier, ws)
     fp64_peak = _native.fp64_peak_tflops(None)
     dmma_peak = _native.dmma_peak_tflops(None)
     if rank != 0:
@@ -350,8 +362,10 @@ def run_ours(args, cfgname):
     fl = stage_flops(cfg, bands)
     dom = max(("leg_synth", "leg_ana"), key=lambda s: prof[s][0])
     dms, dn = prof[dom]
+    # per GPU: the job's FLOPs of the stage per round trip / P, over this rank's
+    # stage time per round trip (the profile pass ran n_prof round trips)
     shard_frac = 1.0 / ws if mode == "shard" else 1.0
-    achieved = fl[dom] * shard_frac / (dms / dn * 1e-3) / 1e12 if dn else None
+    achieved = (fl[dom] * shard_frac / (dms / n_prof * 1e-3) / 1e12) if dms else None
     peak = max(fp64_peak, dmma_peak)
     stages = {k: {"ms_per_step": v[0] / n_prof, "launches_per_step": v[1] / n_prof}
               for k, v in prof.items()}
@@ -375,6 +389,7 @@ def run_ours(args, cfgname):
                 "api": ("ShardedWaveletTransform.round_trip (copies serial)" if mode == "shard" else
                         "WaveletTransform.round_trip_stream (H2D/D2H of neighbouring steps overlap "
                         "the transforms; pinned host buffers)")},
+        "e2e_dropin": dropin,
         "gpu_launches": int(launches),
         "cuda_graph": use_graph,
         "roofline": {
@@ -383,7 +398,9 @@ def run_ours(args, cfgname):
             "frac": achieved / peak if achieved else None,
             "traffic": _traffic(cfgname, dom, mode),
             "traffic_unit": "bytes per launch (DRAM read + write, ncu --set full)",
-            "flops_per_launch": fl[dom] * shard_frac,
+            "flops_per_rt": fl[dom] * shard_frac,
+            "stage_ms_per_rt": dms / n_prof,
+            "launches_per_rt": dn / n_prof,
             "peak_source": f"measured in this run: DFMA {fp64_peak:.1f}, DMMA {dmma_peak:.1f} "
                            "TFLOP/s (s2w_fp64_peak / s2w_dmma_peak); MEASURED_PEAKS.json has "
                            "no FP64 entry",
@@ -404,6 +421,46 @@ def run_ours(args, cfgname):
     if dist.is_initialized():
         dist.destroy_process_group()
     return rec
+
+
+def dropin_e2e(sw, tcfg, x, real, args, barrier, ws):
+    """Round trips/s of the drop-in's host API (run_trial's timed pair), wall
+    clock around K synchronous steps (each call returns host arrays), max
+    over ranks; the batch configs go through the *_batch variants."""
+    import torch
+    import torch.distributed as dist
+
+    grid = sw.make_grid(tcfg.scheme, tcfg.L)
+    vals = x.cpu().numpy()
+    maps = [sw.SphereMap(grid, v.astype(np.complex128), is_real=real) for v in vals]
+    B = len(maps)
+
+    def one():
+        dec = sw.wav_analysis_pixel_batch(maps, tcfg)
+        return dec, sw.wav_synthesis_pixel_batch(dec)
+
+    dec, rec = one()
+    err = max(float(np.abs(r.values - m.values).max()) for r, m in zip(rec, maps))
+    scale_bytes = sum(m.values.size * (8 if real else 16)
+                      for d in dec[:1] for m in (d.scaling, *d.wavelets)) * B
+    map_bytes = B * vals[0].size * (8 if real else 16)
+    k = max(1, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        one()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = t.item()
+    return {"value": ws * B * k / dt, "unit": "round-trips/s", "steps": k,
+            "h2d_bytes_per_step": map_bytes + scale_bytes, "d2h_bytes_per_step": scale_bytes + map_bytes,
+            "max_abs_err": err,
+            "api": "wav_analysis_pixel_batch -> host WaveletDecomposition -> "
+                   "wav_synthesis_pixel_batch (numpy in/out, reference run_trial's timed pair; "
+                   "wall clock, synchronous pageable copies)"}
 
 
 def workload_config(cfgname, bands, mode, ws, map_bytes):

@@ -196,6 +196,28 @@ int s2w_shard_legendre_synthesis(s2w_shard_plan* plan, const double* flm, int fl
 int s2w_shard_legendre_analysis(s2w_shard_plan* plan, const double* H, double* flm, int flm_L,
                                 int w_index, int accumulate, void* stream);
 
+/* Several weighted sets of one grid in one launch (the scales that share
+ * it): synthesis writes G[s] from weight row w_index[s]; analysis folds
+ * sum_s w[s] x analysis(H[s]) into flm in set order.  n <= 3. */
+int s2w_shard_legendre_synthesis_sets(s2w_shard_plan* plan, const double* flm, int flm_L, int n,
+                                      const int* w_index, double* const* G, void* stream);
+int s2w_shard_legendre_analysis_sets(s2w_shard_plan* plan, int n, const double* const* H,
+                                     const int* w_index, double* flm, int flm_L, int accumulate,
+                                     void* stream);
+/* Exchange layout: the P ranks' ring blocks (ring_t0t1[2q], [2q+1], tiling
+ * [0, L) in rank order) and bin lists (n_bins[q] entries each, concatenated in
+ * rank order; `rank`'s must equal this plan's).  Afterwards rings_forward
+ * writes G_col grouped by destination: for q in rank order, [B][n_q][t1-t0]
+ * (one contiguous block per destination, sent as is).  Replaces the
+ * all-to-all packing of distributed.py (round 1). */
+int s2w_shard_set_peers(s2w_shard_plan* plan, int P, int rank, const int* ring_t0t1,
+                        const int* n_bins, const int* bins);
+/* Received blocks [B][n_local][t_q] (src[q], device pointers, HOST array of P)
+ * -> H_local [B][n_local][L]. */
+int s2w_shard_gather_rings(s2w_shard_plan* plan, const double* const* src, double* H, void* stream);
+/* Received blocks [B][t1-t0][n_q] of rank q's bins -> G_ring [B][t1-t0][n_bins]. */
+int s2w_shard_scatter_bins(s2w_shard_plan* plan, const double* const* src, double* G, void* stream);
+
 /* ---------------------------------------------------------------- accounting */
 /* Number of kernels launched by this library since load (bench "gpu_launches"). */
 long long s2w_kernel_launches(void);

@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import warnings
 
 import numpy as np
 
@@ -46,12 +47,15 @@ def ptr(tensor) -> ctypes.c_void_p:
 
 
 def to_device(arr: np.ndarray):
-    """Host numpy -> CUDA tensor through a pinned staging buffer."""
+    """Host numpy -> CUDA tensor.  Pageable source: the driver stages it (a
+    per-call pin_memory() allocation costs more than it saves)."""
     t = torch()
-    host = t.from_numpy(np.require(arr, requirements=["C", "W"]))
-    if host.numel() * host.element_size() >= (1 << 20):
-        host = host.pin_memory()
-    return host.to(device=f"cuda:{device_index()}", non_blocking=True)
+    arr = np.require(arr, requirements=["C"])
+    with warnings.catch_warnings():
+        # read-only inputs (SphereMap values) are only read by the copy
+        warnings.simplefilter("ignore", UserWarning)
+        host = t.from_numpy(arr)
+    return host.to(device=f"cuda:{device_index()}")
 
 
 def to_host(tensor) -> np.ndarray:

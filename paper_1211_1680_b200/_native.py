@@ -65,6 +65,14 @@ _PROTOS = {
     "s2w_shard_theta": (_c_int, [_vp, _vp, _vp]),
     "s2w_shard_legendre_synthesis": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _vp]),
     "s2w_shard_legendre_analysis": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp]),
+    "s2w_shard_legendre_synthesis_sets": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.POINTER(_c_int),
+                                                   ctypes.POINTER(_vp), _vp]),
+    "s2w_shard_legendre_analysis_sets": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp),
+                                                  ctypes.POINTER(_c_int), _vp, _c_int, _c_int, _vp]),
+    "s2w_shard_set_peers": (_c_int, [_vp, _c_int, _c_int, ctypes.POINTER(_c_int),
+                                     ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)]),
+    "s2w_shard_gather_rings": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_shard_scatter_bins": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_kernel_launches": (ctypes.c_longlong, []),
     "s2w_profile_enable": (_c_int, [_c_int]),
     "s2w_profile_read": (
@@ -130,7 +138,7 @@ def version() -> str:
     return load().s2w_version().decode()
 
 
-N_STAGES = 6
+N_STAGES = 7
 
 
 def kernel_launches() -> int:

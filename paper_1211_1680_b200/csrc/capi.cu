@@ -118,9 +118,9 @@ struct DevBuf {
 #include <atomic>
 static std::atomic<long long> g_launches{0};
 
-enum ProfStage { P_LEG_SYNTH = 0, P_LEG_ANA, P_PHI_FWD, P_THETA, P_PHI_INV, P_TILE, P_NSTAGE };
+enum ProfStage { P_LEG_SYNTH = 0, P_LEG_ANA, P_PHI_FWD, P_THETA, P_PHI_INV, P_TILE, P_XCHG, P_NSTAGE };
 static const char* kStageNames[P_NSTAGE] = {"leg_synth", "leg_ana", "phi_fwd",
-                                            "theta", "phi_inv", "tile"};
+                                            "theta", "phi_inv", "tile", "xchg_layout"};
 struct ProfRec {
   int stage;
   cudaEvent_t a, b;

@@ -92,17 +92,16 @@ __global__ void __launch_bounds__(fft_maxthr(LOGM), fft_minb(LOGM)) phi_fwd_kern
   __syncthreads();
   fft_conv<LOGM, GS>(buf, tw, T.bl_fwd, gtid);
   if (!valid) return;
-  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
   for (int mi = gtid; mi < a.n_bins; mi += GS) {
     const double2 z = cmul(__ldg(&T.chirp[mi]), buf[swz(mi)]);
     if (!a.real) {
-      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+      fwd_row(a, set, mi)[ta] = cscale(z, a.scale);
     } else {
       const int mr = mi ? N - mi : 0;
       const double2 zr = cconj(cmul(__ldg(&T.chirp[mr]), buf[swz(mr)]));
       const double h = 0.5 * a.scale;
-      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
-      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
+      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
     }
   }
 }
@@ -205,16 +204,15 @@ __global__ void __launch_bounds__(PFA_T) phi_fwd_pfa_kernel(PhiFwdArgs a) {
   }
   __syncthreads();
   pfa4095<false>(buf, tid, PFA_T);
-  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
   for (int mi = tid; mi < a.n_bins; mi += PFA_T) {
     const double2 z = buf[pfa_pos(mi)];
     if (!a.real) {
-      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+      fwd_row(a, set, mi)[ta] = cscale(z, a.scale);
     } else {
       const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
       const double h = 0.5 * a.scale;
-      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
-      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
+      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
     }
   }
 }
@@ -583,19 +581,18 @@ __global__ void __launch_bounds__(SPLIT_T) phi_fwd_split_kernel(PhiFwdArgs a) {
         buf[swz(j)] = v;
       }
     });
-    double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
     for (int mi = threadIdx.x; mi < a.n_bins; mi += SPLIT_T) {
       const double2 y = cadd(u[mi], cmulc(buf[swz(mi)], wM(mi, octM, logM)));
       const double2 z = cmul(__ldg(&T.chirp[mi]), y);
       if (!a.real) {
-        out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+        fwd_row(a, set, mi)[ta] = cscale(z, a.scale);
       } else {
         const int mr = mi ? N - mi : 0;
         const double2 yr = cadd(u[mr], cmulc(buf[swz(mr)], wM(mr, octM, logM)));
         const double2 zr = cconj(cmul(__ldg(&T.chirp[mr]), yr));
         const double h = 0.5 * a.scale;
-        out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
-        if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+        fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
+        if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
       }
     }
     __syncthreads();
@@ -903,16 +900,15 @@ __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB) phi_fwd_k2_kernel(PhiFwdAr
     __syncthreads();
   }
   pfa4095<false>(buf, tid, T);
-  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
   for (int mi = tid; mi < a.n_bins; mi += T) {
     const double2 z = buf[pfa_pos(mi)];
     if (!a.real) {
-      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+      fwd_row(a, set, mi)[ta] = cscale(z, a.scale);
     } else {
       const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
       const double h = 0.5 * a.scale;
-      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
-      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
+      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
     }
   }
 }
@@ -1120,16 +1116,15 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
   const RaderTabs R = rader_tabs(a.T);
   double2 x0, X0;
   rader8191<T, false>(buf, R, part, x0, X0);
-  double2* out = a.out + (size_t)set * a.n_bins * a.n_rings;
   for (int mi = tid; mi < a.n_bins; mi += T) {
     const double2 z = rader_bin<false>(buf, R, x0, X0, mi);
     if (!a.real) {
-      out[(size_t)mi * a.n_rings + ta] = cscale(z, a.scale);
+      fwd_row(a, set, mi)[ta] = cscale(z, a.scale);
     } else {
       const double2 zr = cconj(rader_bin<false>(buf, R, x0, X0, mi ? N - mi : 0));
       const double h = 0.5 * a.scale;
-      out[(size_t)mi * a.n_rings + ta] = cscale(cadd(z, zr), h);
-      if (vb) out[(size_t)mi * a.n_rings + ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
+      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
     }
   }
 }

@@ -57,7 +57,17 @@ struct PhiFwdArgs {
   int gsize, rpc;  // filled by the launcher
   double2* scratch;  // split mode: per-CTA scratch (fft_split_scratch_elems)
   int pfd = 0;  // k2 kernels: rows ahead whose input a CTA prefetches into L2 (launcher)
+  // optional output row offsets (double2 elements) per (set, bin): the shard
+  // plans write each destination rank's bins as one contiguous block
+  // (s2w_shard_set_peers); nullptr = [set][mi][ring]
+  const long long* ofs = nullptr;
 };
+
+// start of the output row of (set, bin mi) of a forward ring-DFT launch
+__device__ __forceinline__ double2* fwd_row(const PhiFwdArgs& a, int set, int mi) {
+  return a.ofs ? a.out + a.ofs[(size_t)set * a.n_bins + mi]
+               : a.out + ((size_t)set * a.n_bins + mi) * a.n_rings;
+}
 
 struct PhiInvArgs {
   FftTablesDev T;
@@ -238,5 +248,19 @@ cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st);
 cudaError_t measure_fp64_peak(double* tflops, cudaStream_t st);
 // FP64 tensor-core (mma.sync m8n8k4 DMMA) throughput in TFLOP/s.
 cudaError_t measure_dmma_peak(double* tflops, cudaStream_t st);
+
+// ------------------------------------------------------------------ shard exchange layouts
+constexpr int S2W_MAX_RANKS = 16;
+struct ShardSrc {
+  const double2* p[S2W_MAX_RANKS];  // received block per source rank
+};
+// blocks [B][n_local][t_q] per source -> H [B][n_local][L]; ring_src[t] = (q, t - t0_q),
+// t_len[q] = ring count of q's block
+cudaError_t launch_shard_gather_rings(const ShardSrc& src, const int2* ring_src, const int* t_len,
+                                      int B, int n_local, int L, double2* H, cudaStream_t st);
+// blocks [B][t_r][n_q] per source -> G [B][t_r][n_bins]; bin_src[bin] = (q, index in q's bins),
+// n_src[q] = number of q's bins
+cudaError_t launch_shard_scatter_bins(const ShardSrc& src, const int2* bin_src, const int* n_src,
+                                      int B, int t_r, int n_bins, double2* G, cudaStream_t st);
 
 }  // namespace s2w

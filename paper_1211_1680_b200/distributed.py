@@ -8,18 +8,31 @@ Partition (one process per GPU, torch.distributed over NCCL):
   the SHTs of a wavelet transform is rank-local;
 * the ring FFT stages are split **by ring**: every rank owns a contiguous
   block of rings of each grid (its slice of the input / output maps);
-* between the two, one all-to-all per grid moves the per-ring Fourier modes
+* between the two, an all-to-all exchange of the per-ring Fourier modes
   G_m(theta_t): analysis ring-block x all-orders -> all-rings x my-orders;
   synthesis the reverse.  Message size per SHT is k (2k-1) 16 B in total
   (134 MB for C4's L = 2048), i.e. ~20 us over NVLink 5 against milliseconds
-  of FP64 work.
+  of FP64 work (DESIGN.md section 7 tabulates the bytes per rank).
 
-All arithmetic runs in libs2w.so (C ABI ``s2w_shard_*``); this module only
-builds the partition, packs / unpacks exchange buffers with torch indexing
-and calls the exchanger.  Two exchangers exist: ``TorchExchange``
-(torch.distributed ``all_to_all_single``; NCCL on GPUs, gloo on CPU) and
-``VirtualExchange`` (several ranks in one process, for single-GPU testing:
-ranks run stage by stage and never wait on one another).
+Small scales are not sharded: a scale whose band is at most ``whole_max``
+(256) runs whole on one rank (owners dealt by cost, largest first), on the
+low-degree block of f_lm that one all-reduce (B k_s^2 16 B, k_s the largest
+such band: 1 MB at C4) makes complete on every rank.  Their maps live whole on
+the owner; the synthesis folds them back with a second all-reduce.  The large
+scales and the map itself are order/ring sharded, and all large scales of a
+direction share ONE grouped exchange (per destination, one message per
+scale, in a single NCCL group): per round trip 4 exchanges + 2 small
+all-reduces, whatever the number of scales.
+
+All arithmetic runs in libs2w.so (C ABI ``s2w_shard_*``).  No packing: the
+forward ring DFTs write each destination's bins as one contiguous block
+(``s2w_shard_set_peers``), the Legendre synthesis writes ring-major rows whose
+ring blocks are contiguous, and the receive side places the blocks with
+``s2w_shard_gather_rings`` / ``s2w_shard_scatter_bins`` (a rank's own block is
+read straight from its send buffer).  Exchangers: ``TorchExchange``
+(torch.distributed grouped P2P, ``batch_isend_irecv``: NCCL on GPUs, gloo on
+CPU) and ``VirtualExchange`` (several ranks in one process, for single-GPU
+testing: delivery by reference, ranks never wait on one another).
 """
 from __future__ import annotations
 
@@ -80,7 +93,7 @@ def shard_bins(k: int, orders, real: bool) -> np.ndarray:
 
 # ---------------------------------------------------------------- exchangers
 class TorchExchange:
-    """all-to-all through torch.distributed (one rank per process)."""
+    """Grouped point-to-point exchange through torch.distributed (one rank per process)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -89,14 +102,50 @@ class TorchExchange:
         self.P = dist.get_world_size(group)
         self.ranks = [dist.get_rank(group)]
 
+    def exchange(self, sends: dict, recv_shapes: dict) -> dict:
+        """sends[rank][key][dst] -> contiguous tensor for dst (None: nothing);
+        recv_shapes[rank][key][src] -> shape of what src sends (None: nothing).
+        Returns got[rank][key][src]: the received tensor (a rank's own block is
+        its send tensor, not copied).  All messages of the call form one group
+        (one NCCL launch); messages between a pair match in key order."""
+        th = _device.torch()
+        (me,) = self.ranks
+        ops, got = [], {}
+        for key in sorted(sends[me]):
+            out, shapes = sends[me][key], recv_shapes[me][key]
+            row = []
+            for q in range(self.P):
+                if q == me:
+                    row.append(out[q])
+                    continue
+                if out[q] is not None and out[q].numel():
+                    ops.append(self.dist.P2POp(self.dist.isend, _real_view(out[q]), q, self.group))
+                rb = None
+                if shapes[q] is not None and math.prod(shapes[q]):
+                    rb = th.empty(shapes[q], dtype=out_dtype(sends[me][key]), device=_dev_of(sends[me][key]))
+                    ops.append(self.dist.P2POp(self.dist.irecv, _real_view(rb), q, self.group))
+                row.append(rb)
+            got[key] = row
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        return {me: got}
+
+    def all_reduce(self, bufs: dict) -> None:
+        """In-place sum over ranks."""
+        (me,) = self.ranks
+        t = bufs[me]
+        if t.numel():
+            self.dist.all_reduce(_real_view(t), group=self.group)
+
     def all_to_all(self, sends: dict, recv_sizes: dict) -> dict:
-        """sends[rank][dst] -> tensors; recv_sizes[rank][src] element counts
-        (known from the partition); returns recvs[rank][src] (flat)."""
+        """Flat all-to-all (sends[rank][dst] -> tensors; recv_sizes[rank][src]
+        element counts); returns recvs[rank][src] (flat).  Kept for callers
+        that exchange host-computed blocks."""
         th = _device.torch()
         (me,) = self.ranks
         out = sends[me]
         cplx = out[0].is_complex()
-        # complex payloads travel as interleaved float64 (NCCL / gloo have no complex type)
         flat = [th.view_as_real(t).reshape(-1) if cplx else t.reshape(-1) for t in out]
         w = 2 if cplx else 1
         in_splits = [int(t.numel()) for t in flat]
@@ -110,6 +159,26 @@ class TorchExchange:
         return {me: list(parts)}
 
 
+def _real_view(t):
+    """NCCL / gloo have no complex type: complex payloads travel as float64 pairs."""
+    th = _device.torch()
+    return th.view_as_real(t) if t.is_complex() else t
+
+
+def out_dtype(row):
+    for t in row:
+        if t is not None:
+            return t.dtype
+    raise ParameterError("exchange row without any tensor")
+
+
+def _dev_of(row):
+    for t in row:
+        if t is not None:
+            return t.device
+    raise ParameterError("exchange row without any tensor")
+
+
 class VirtualExchange:
     """P ranks in one process (single-GPU testing): delivery by reference."""
 
@@ -117,11 +186,28 @@ class VirtualExchange:
         self.P = P
         self.ranks = list(range(P))
 
+    def exchange(self, sends: dict, recv_shapes: dict = None) -> dict:
+        return {r: {key: [sends[q][key][r] for q in range(self.P)] for key in sends[r]}
+                for r in self.ranks}
+
+    def all_reduce(self, bufs: dict) -> None:
+        total = None
+        for r in self.ranks:
+            total = bufs[r].clone() if total is None else total + bufs[r]
+        for r in self.ranks:
+            bufs[r].copy_(total)
+
     def all_to_all(self, sends: dict, recv_sizes: dict = None) -> dict:
         return {r: [sends[q][r].reshape(-1) for q in range(self.P)] for r in self.ranks}
 
 
 # ---------------------------------------------------------------- GPU backend
+def _ptrs(tensors):
+    arr = (ctypes.c_void_p * len(tensors))(
+        *[(t.data_ptr() if t is not None and t.numel() else 0) for t in tensors])
+    return arr
+
+
 class _GpuShard:
     """C-ABI shard plan of one grid for one rank."""
 
@@ -136,6 +222,16 @@ class _GpuShard:
             scheme_code(scheme), k, batch, int(real), int(orders.size), oc, t0, t1,
             0 if w is None else w.shape[0], wp, _device.device_index(), ctypes.byref(h)))
         self.h, self.lib = h, lib
+
+    def set_peers(self, rank, blocks, bins):
+        t = np.ascontiguousarray(np.asarray(blocks, dtype=np.int32).reshape(-1))
+        n = np.ascontiguousarray([len(b) for b in bins], dtype=np.int32)
+        cat = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int32) for b in bins])
+                                   if sum(n) else np.zeros(1, np.int32))
+        ip = ctypes.POINTER(ctypes.c_int)
+        _native.check(self.lib.s2w_shard_set_peers(
+            self.h, len(bins), rank, t.ctypes.data_as(ip), n.ctypes.data_as(ip),
+            cat.ctypes.data_as(ip)))
 
     def __del__(self):
         try:
@@ -154,18 +250,37 @@ class _Grid:
     orders: list            # np.ndarray of orders per rank
     bins: list              # local bins per rank
     plans: dict             # rank -> _GpuShard (unweighted)
-    wplans: dict            # (rank, scale j) -> _GpuShard with weight row 0 = fac_j
+    wplans: dict            # rank -> _GpuShard, weight row i = fac of the grid's i-th large scale
+
+
+_SETS_MAX = 3  # weighted sets per shard Legendre launch (s2w_shard_legendre_*_sets)
+
+
+def whole_scale_owners(bands, P: int, whole_max: int = 256) -> dict:
+    """Scales with band <= whole_max, dealt whole to ranks: largest band first,
+    each to the least loaded rank (cost ~ k^3).  {scale j: rank}."""
+    load = np.zeros(P)
+    own = {}
+    for j in sorted((j for j, k in enumerate(bands) if k <= whole_max), key=lambda j: (-bands[j], j)):
+        r = int(np.argmin(load))
+        own[j] = r
+        load[r] += float(bands[j]) ** 3
+    return own
 
 
 class ShardedWaveletTransform:
     """Wavelet analysis / synthesis of one map sharded over P ranks.
 
-    Inputs and outputs are the rank-local ring blocks of the maps:
-    ``analysis({rank: x_rows})`` with x_rows of shape (batch, t1 - t0, 2L-1)
-    returns ``{rank: [rows of scale map j]}``; ``synthesis`` is the inverse.
+    The map and the large scale maps are ring-sharded: ``analysis({rank:
+    x_rows})`` with x_rows of shape (batch, t1 - t0, 2L-1) (``ring_block``)
+    returns ``{rank: [scale map j]}`` where a large scale's entry is the rank's
+    ring block and a whole scale's (band <= whole_max, ``whole_owner``) is the
+    full map on its owner and an empty (batch, 0, 2k-1) tensor elsewhere;
+    ``synthesis`` takes the same layout back.
     """
 
-    def __init__(self, config: TransformConfig, exchange, batch: int = 1, real: bool = False):
+    def __init__(self, config: TransformConfig, exchange, batch: int = 1, real: bool = False,
+                 whole_max: int = 256):
         _device.require_cuda()
         self.cfg, self.ex, self.B, self.real = config, exchange, batch, bool(real)
         self.P = exchange.P
@@ -176,28 +291,50 @@ class ShardedWaveletTransform:
         self.fac = np.sqrt(4.0 * np.pi / (2.0 * ell + 1.0))[None, :] * kern.table()
         owner = order_owner(L, self.P)
         self.owner = owner
+        self.whole_owner = whole_scale_owners(self.bands, self.P, whole_max)
+        self.large = [j for j in range(len(self.bands)) if j not in self.whole_owner]
+        self.ks = max([self.bands[j] for j in self.whole_owner], default=0)
         self.grids = {}
-        for k in sorted(set([L, *self.bands])):
+        for k in sorted(set([L] + [self.bands[j] for j in self.large])):
             blocks = ring_blocks(k, self.P)
             orders = [np.nonzero(owner[:k] == r)[0] for r in range(self.P)]
             bins = [shard_bins(k, o, self.real) for o in orders]
-            self.grids[k] = _Grid(k, blocks, orders, bins, {}, {})
+            g = _Grid(k, blocks, orders, bins, {}, {})
+            self.grids[k] = g
             for r in exchange.ranks:
                 t0, t1 = blocks[r]
-                self.grids[k].plans[r] = _GpuShard(config.scheme, k, batch, real, orders[r], t0, t1,
-                                                    None)
-        for j, k in enumerate(self.bands):
+                g.plans[r] = _GpuShard(config.scheme, k, batch, real, orders[r], t0, t1, None)
+                g.plans[r].set_peers(r, blocks, bins)
+        # one weighted plan per (rank, large grid): weight row i = fac of the
+        # grid's i-th scale, so the scales sharing a grid run as one launch
+        self.large_groups = {}
+        for j in self.large:
+            self.large_groups.setdefault(self.bands[j], []).append(j)
+        for k, js in self.large_groups.items():
             g = self.grids[k]
             for r in exchange.ranks:
                 t0, t1 = g.blocks[r]
-                g.wplans[(r, j)] = _GpuShard(config.scheme, k, batch, real, g.orders[r], t0, t1,
-                                             self.fac[j:j + 1, :k])
+                p = _GpuShard(config.scheme, k, batch, real, g.orders[r], t0, t1,
+                              self.fac[js, :k])
+                p.set_peers(r, g.blocks, g.bins)
+                g.wplans[r] = p
+        # whole scales: the owner's plan holds every order and every ring
+        self.wholeplans = {}
+        for j, r in self.whole_owner.items():
+            if r in exchange.ranks:
+                k = self.bands[j]
+                p = _GpuShard(config.scheme, k, batch, real, np.arange(k), 0, k,
+                              self.fac[j:j + 1, :k])
+                # one "rank" holding everything: local bin order for the ring DFTs,
+                # natural order back through scatter_bins
+                p.set_peers(0, [(0, k)], [shard_bins(k, np.arange(k), self.real)])
+                self.wholeplans[j] = p
         th = _device.torch()
         self.dev = f"cuda:{_device.device_index()}"
-        self._bins_t = {k: [th.as_tensor(b, device=self.dev) for b in g.bins]
-                        for k, g in self.grids.items()}
         self.f = {r: th.zeros((batch, L * L), dtype=th.complex128, device=self.dev)
                   for r in exchange.ranks}
+        self.flow = {r: th.zeros((batch, self.ks * self.ks), dtype=th.complex128, device=self.dev)
+                     for r in exchange.ranks}
 
     # -- helpers
     def _nb(self, k):
@@ -206,107 +343,192 @@ class ShardedWaveletTransform:
     def _stream(self):
         return _device.stream_handle()
 
-    def _cols_to_local(self, k, gcol: dict) -> dict:
-        """G_col[r] (B, n_bins, t_r) -> H_local[r] (B, n_local_r, k) via all-to-all."""
+    def _map_dtype(self):
         th = _device.torch()
-        g = self.grids[k]
-        sends = {r: [gcol[r][:, self._bins_t[k][q], :].contiguous() for q in range(self.P)]
-                 for r in self.ex.ranks}
-        sizes = {r: [self.B * len(g.bins[r]) * (g.blocks[q][1] - g.blocks[q][0])
-                     for q in range(self.P)] for r in self.ex.ranks}
-        recv = self.ex.all_to_all(sends, sizes)
+        return th.float64 if self.real else th.complex128
+
+    def _forward_many(self, items: list) -> dict:
+        """items: [(key, k, plan_of(r), {rank: map rows})] -> {rank: {key: H_local}}
+        (ring DFTs of my rings, ONE grouped exchange, MW theta stage)."""
+        th = _device.torch()
+        sends, shapes, gcols = {}, {}, {}
+        for r in self.ex.ranks:
+            sends[r], shapes[r], gcols[r] = {}, {}, {}
+            for key, k, plan_of, rows in items:
+                g = self.grids[k]
+                t = g.blocks[r][1] - g.blocks[r][0]
+                gc = th.empty(self.B * self._nb(k) * t, dtype=th.complex128, device=self.dev)
+                plan_of(r).call("s2w_shard_rings_forward", _device.ptr(rows[r]), _device.ptr(gc),
+                                self._stream())
+                gcols[r][key] = gc
+                # destination-grouped blocks [B][n_q][t_r]: views, no packing
+                parts, o = [], 0
+                for q in range(self.P):
+                    n = self.B * len(g.bins[q]) * t
+                    parts.append(gc[o:o + n].view(self.B, len(g.bins[q]), t))
+                    o += n
+                sends[r][key] = parts
+                shapes[r][key] = [(self.B, len(g.bins[r]), g.blocks[q][1] - g.blocks[q][0])
+                                  for q in range(self.P)]
+        got = self.ex.exchange(sends, shapes)
         out = {}
         for r in self.ex.ranks:
-            nl = len(g.bins[r])
-            parts = [recv[r][q].view(self.B, nl, g.blocks[q][1] - g.blocks[q][0])
-                     for q in range(self.P)]
-            out[r] = th.cat(parts, dim=2).contiguous()
+            out[r] = {}
+            for key, k, plan_of, _ in items:
+                g = self.grids[k]
+                if self.P == 1:
+                    # one rank: its destination block [B][n_local][k] is H itself
+                    H = got[r][key][0]
+                else:
+                    H = th.empty((self.B, len(g.bins[r]), k), dtype=th.complex128, device=self.dev)
+                    if len(g.bins[r]):
+                        plan_of(r).call("s2w_shard_gather_rings", _ptrs(got[r][key]),
+                                        _device.ptr(H), self._stream())
+                if len(g.bins[r]):
+                    plan_of(r).call("s2w_shard_theta", _device.ptr(H), self._stream())
+                out[r][key] = H
         return out
 
-    def _local_to_rings(self, k, glocal: dict) -> dict:
-        """G_local[r] (B, k, n_local_r) -> G_ring[r] (B, t_r, n_bins) via all-to-all."""
+    def _inverse_many(self, items: list) -> dict:
+        """items: [(key, k, plan_of(r), {rank: G_local [B][k][n_local]})] ->
+        {rank: {key: map rows}} (ONE grouped exchange, ring inverse DFTs)."""
         th = _device.torch()
-        g = self.grids[k]
-        sends = {r: [glocal[r][:, g.blocks[q][0]:g.blocks[q][1], :].contiguous()
-                     for q in range(self.P)] for r in self.ex.ranks}
-        sizes = {r: [self.B * (g.blocks[r][1] - g.blocks[r][0]) * len(g.bins[q])
-                     for q in range(self.P)] for r in self.ex.ranks}
-        recv = self.ex.all_to_all(sends, sizes)
+        sends, shapes = {}, {}
+        for r in self.ex.ranks:
+            sends[r], shapes[r] = {}, {}
+            for key, k, _, gl in items:
+                g = self.grids[k]
+                G = gl[r]
+                # ring-major rows: each destination's ring block is contiguous per set
+                if self.B == 1:
+                    sends[r][key] = [G[:, g.blocks[q][0]:g.blocks[q][1], :] for q in range(self.P)]
+                else:
+                    sends[r][key] = [G[:, g.blocks[q][0]:g.blocks[q][1], :].contiguous()
+                                     for q in range(self.P)]
+                t = g.blocks[r][1] - g.blocks[r][0]
+                shapes[r][key] = [(self.B, t, len(g.bins[q])) for q in range(self.P)]
+        got = self.ex.exchange(sends, shapes)
         out = {}
         for r in self.ex.ranks:
-            t = g.blocks[r][1] - g.blocks[r][0]
-            ring = th.zeros((self.B, t, self._nb(k)), dtype=th.complex128, device=self.dev)
-            for q in range(self.P):
-                nl = len(g.bins[q])
-                if nl:
-                    ring[:, :, self._bins_t[k][q]] = recv[r][q].view(self.B, t, nl)
-            out[r] = ring
+            out[r] = {}
+            for key, k, plan_of, _ in items:
+                g = self.grids[k]
+                t = g.blocks[r][1] - g.blocks[r][0]
+                ring = th.empty((self.B, t, self._nb(k)), dtype=th.complex128, device=self.dev)
+                x = th.empty((self.B, t, 2 * k - 1), dtype=self._map_dtype(), device=self.dev)
+                if t:
+                    plan_of(r).call("s2w_shard_scatter_bins", _ptrs(got[r][key]), _device.ptr(ring),
+                                    self._stream())
+                    plan_of(r).call("s2w_shard_rings_inverse", _device.ptr(ring), _device.ptr(x),
+                                    self._stream())
+                out[r][key] = x
         return out
 
-    def _forward(self, k, rows: dict) -> dict:
-        """map rows -> H_local (theta stage applied on MW)."""
+    def _empty_map(self, k):
         th = _device.torch()
-        g = self.grids[k]
-        gcol = {}
-        for r in self.ex.ranks:
-            t = g.blocks[r][1] - g.blocks[r][0]
-            gc = th.empty((self.B, self._nb(k), t), dtype=th.complex128, device=self.dev)
-            g.plans[r].call("s2w_shard_rings_forward", _device.ptr(rows[r]), _device.ptr(gc),
-                            self._stream())
-            gcol[r] = gc
-        H = self._cols_to_local(k, gcol)
-        for r in self.ex.ranks:
-            if len(g.bins[r]):
-                g.plans[r].call("s2w_shard_theta", _device.ptr(H[r]), self._stream())
-        return H
-
-    def _inverse(self, k, glocal: dict) -> dict:
-        th = _device.torch()
-        g = self.grids[k]
-        ring = self._local_to_rings(k, glocal)
-        out = {}
-        for r in self.ex.ranks:
-            t = g.blocks[r][1] - g.blocks[r][0]
-            x = th.empty((self.B, t, 2 * k - 1), dtype=th.float64 if self.real else th.complex128,
-                         device=self.dev)
-            g.plans[r].call("s2w_shard_rings_inverse", _device.ptr(ring[r]), _device.ptr(x),
-                            self._stream())
-            out[r] = x
-        return out
+        return th.empty((self.B, 0, 2 * k - 1), dtype=self._map_dtype(), device=self.dev)
 
     # -- public
     def analysis(self, x_rows: dict) -> dict:
         th = _device.torch()
         L = self.cfg.L
-        H = self._forward(L, x_rows)
         top = self.grids[L]
+        H = self._forward_many([("top", L, lambda r: top.plans[r], x_rows)])
         for r in self.ex.ranks:
-            top.plans[r].call("s2w_shard_legendre_analysis", _device.ptr(H[r]),
+            top.plans[r].call("s2w_shard_legendre_analysis", _device.ptr(H[r]["top"]),
                               _device.ptr(self.f[r]), L, -1, 0, self._stream())
-        out = {r: [] for r in self.ex.ranks}
-        for j, k in enumerate(self.bands):
+        out = {r: [None] * len(self.bands) for r in self.ex.ranks}
+        # whole scales: complete low-degree f on every rank (one all-reduce)
+        if self.whole_owner:
+            ks = self.ks
+            for r in self.ex.ranks:
+                self.flow[r].copy_(self.f[r][:, :ks * ks])
+            self.ex.all_reduce(self.flow)
+            for j, k in enumerate(self.bands):
+                if j not in self.whole_owner:
+                    continue
+                for r in self.ex.ranks:
+                    if self.whole_owner[j] != r:
+                        out[r][j] = self._empty_map(k)
+                        continue
+                    p = self.wholeplans[j]
+                    G = th.empty((self.B, k, self._nb(k)), dtype=th.complex128, device=self.dev)
+                    p.call("s2w_shard_legendre_synthesis", _device.ptr(self.flow[r]), ks, 0,
+                           _device.ptr(G), self._stream())
+                    ring = th.empty_like(G)
+                    p.call("s2w_shard_scatter_bins", _ptrs([G]), _device.ptr(ring), self._stream())
+                    x = th.empty((self.B, k, 2 * k - 1), dtype=self._map_dtype(), device=self.dev)
+                    p.call("s2w_shard_rings_inverse", _device.ptr(ring), _device.ptr(x),
+                           self._stream())
+                    out[r][j] = x
+        # large scales: order-sharded synthesis, ONE grouped exchange, ring inverse
+        items = []
+        for k, js in self.large_groups.items():
             g = self.grids[k]
-            gl = {}
+            gls = {j: {} for j in js}
             for r in self.ex.ranks:
-                G = th.empty((self.B, k, len(g.bins[r])), dtype=th.complex128, device=self.dev)
+                Gs = [th.empty((self.B, k, len(g.bins[r])), dtype=th.complex128, device=self.dev)
+                      for _ in js]
                 if len(g.bins[r]):
-                    g.wplans[(r, j)].call("s2w_shard_legendre_synthesis", _device.ptr(self.f[r]),
-                                          L, 0, _device.ptr(G), self._stream())
-                gl[r] = G
-            maps = self._inverse(k, gl)
+                    for c0 in range(0, len(js), _SETS_MAX):  # <= 3 sets per launch
+                        n = min(_SETS_MAX, len(js) - c0)
+                        w = (ctypes.c_int * n)(*range(c0, c0 + n))
+                        g.wplans[r].call("s2w_shard_legendre_synthesis_sets",
+                                         _device.ptr(self.f[r]), L, n, w, _ptrs(Gs[c0:c0 + n]),
+                                         self._stream())
+                for j, G in zip(js, Gs):
+                    gls[j][r] = G
+            for j in js:
+                items.append((f"s{j:03d}", k, (lambda g_: lambda r: g_.wplans[r])(g), gls[j]))
+        maps = self._inverse_many(items) if items else {r: {} for r in self.ex.ranks}
+        for j in self.large:
             for r in self.ex.ranks:
-                out[r].append(maps[r])
+                out[r][j] = maps[r][f"s{j:03d}"]
         return out
 
     def synthesis(self, scale_rows: dict) -> dict:
         th = _device.torch()
         L = self.cfg.L
-        for j, k in enumerate(self.bands):
-            g = self.grids[k]
-            H = self._forward(k, {r: scale_rows[r][j] for r in self.ex.ranks})
+        # whole scales on their owners, folded in scale order, then one all-reduce
+        for r in self.ex.ranks:
+            self.f[r].zero_()
+        if self.whole_owner:
+            ks = self.ks
             for r in self.ex.ranks:
-                g.wplans[(r, j)].call("s2w_shard_legendre_analysis", _device.ptr(H[r]),
-                                      _device.ptr(self.f[r]), L, 0, int(j > 0), self._stream())
+                self.flow[r].zero_()
+            for j in sorted(self.whole_owner):
+                r = self.whole_owner[j]
+                if r not in self.ex.ranks:
+                    continue
+                k = self.bands[j]
+                p = self.wholeplans[j]
+                H = th.empty((self.B, self._nb(k), k), dtype=th.complex128, device=self.dev)
+                p.call("s2w_shard_rings_forward", _device.ptr(scale_rows[r][j]), _device.ptr(H),
+                       self._stream())
+                p.call("s2w_shard_theta", _device.ptr(H), self._stream())
+                p.call("s2w_shard_legendre_analysis", _device.ptr(H), _device.ptr(self.flow[r]),
+                       ks, 0, 1, self._stream())
+            self.ex.all_reduce(self.flow)
+            for r in self.ex.ranks:
+                self.f[r][:, :ks * ks].copy_(self.flow[r])
+        # large scales: ring DFTs, ONE grouped exchange, order-sharded analysis
+        items = []
+        for j in self.large:
+            k = self.bands[j]
+            g = self.grids[k]
+            items.append((f"s{j:03d}", k, (lambda g_: lambda r: g_.wplans[r])(g),
+                          {r: scale_rows[r][j] for r in self.ex.ranks}))
+        H = self._forward_many(items) if items else {r: {} for r in self.ex.ranks}
+        # grids in increasing band = scale order; a grid's scales fold in one launch
+        for k, js in self.large_groups.items():
+            g = self.grids[k]
+            for r in self.ex.ranks:
+                for c0 in range(0, len(js), _SETS_MAX):  # <= 3 sets per launch, in order
+                    n = min(_SETS_MAX, len(js) - c0)
+                    w = (ctypes.c_int * n)(*range(c0, c0 + n))
+                    g.wplans[r].call("s2w_shard_legendre_analysis_sets", n,
+                                     _ptrs([H[r][f"s{j:03d}"] for j in js[c0:c0 + n]]), w,
+                                     _device.ptr(self.f[r]), L, 1, self._stream())
         top = self.grids[L]
         gl = {}
         for r in self.ex.ranks:
@@ -315,10 +537,29 @@ class ShardedWaveletTransform:
                 top.plans[r].call("s2w_shard_legendre_synthesis", _device.ptr(self.f[r]), L, -1,
                                   _device.ptr(G), self._stream())
             gl[r] = G
-        return self._inverse(L, gl)
+        rows = self._inverse_many([("top", L, lambda r: top.plans[r], gl)])
+        return {r: rows[r]["top"] for r in self.ex.ranks}
 
     def round_trip(self, x_rows: dict) -> dict:
         return self.synthesis(self.analysis(x_rows))
 
     def ring_block(self, k: int, rank: int) -> tuple[int, int]:
-        return self.grids[k].blocks[rank]
+        return ring_blocks(k, self.P)[rank]
+
+    def exchange_bytes(self) -> dict:
+        """Bytes that leave each rank per exchange of one round trip (the
+        all-to-alls move G / H blocks of complex128; own blocks stay local)."""
+        L, B = self.cfg.L, self.B
+
+        def a2a(k):
+            g = ring_blocks(k, self.P)
+            orders = [np.nonzero(self.owner[:k] == r)[0] for r in range(self.P)]
+            nb = [len(shard_bins(k, o, self.real)) for o in orders]
+            per = [sum(B * nb[q] * (g[r][1] - g[r][0]) * 16 for q in range(self.P) if q != r)
+                   for r in range(self.P)]
+            return max(per)
+
+        large = sum(a2a(self.bands[j]) for j in self.large)
+        ar = B * self.ks * self.ks * 16
+        return {"top_a2a": a2a(L), "large_scales_a2a": large, "whole_allreduce": ar,
+                "per_round_trip_max_rank": 2 * a2a(L) + 2 * large + 2 * ar}

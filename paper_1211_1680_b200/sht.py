@@ -158,7 +158,10 @@ def analysis_device(map_dev, n_sets: int, real: bool, grid: GridSpec):
 
 
 def maps_to_device(smaps, real: bool):
-    if real:
+    if len(smaps) == 1:  # no stacking copy for a single map
+        v = smaps[0].values
+        host = np.ascontiguousarray(v.real) if real else v.view(np.float64)
+    elif real:
         host = np.stack([m.values.real for m in smaps])
     else:
         host = np.stack([m.values for m in smaps]).view(np.float64)

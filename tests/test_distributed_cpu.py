@@ -103,3 +103,61 @@ def test_two_rank_sharded_sht(scheme, real):
         if t1 > t0:
             assert np.abs(rows - full_map[:, t0:t1]).max() <= 1e-12
     assert np.abs(got_f - f).max() <= 1e-10
+
+
+def _xchg_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1211_1680_b200 import distributed as D
+
+        ex = D.TorchExchange()
+        # two keys (two scales of one grouped exchange), blocks of rank-dependent shape
+        sends, shapes = {}, {}
+        for key, rows in (("s000", 3), ("s001", 2)):
+            sends[key] = [torch.full((1, rows + d, 2), complex(10 * rank + d, key == "s001"),
+                                     dtype=torch.complex128) for d in range(world)]
+            shapes[key] = [(1, rows + rank, 2) for src in range(world)]
+        got = ex.exchange({rank: sends}, {rank: shapes})[rank]
+        ok = True
+        for key in ("s000", "s001"):
+            for src in range(world):
+                want = complex(10 * src + rank, key == "s001")
+                t = got[key][src]
+                ok &= bool(torch.all(t == want).item()) and tuple(t.shape)[1] == (3 if key == "s000" else 2) + rank
+        buf = torch.full((5,), complex(rank + 1, -rank), dtype=torch.complex128)
+        ex.all_reduce({rank: buf})
+        ok &= bool(torch.all(buf == complex(3, -1)).item())
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grouped_exchange_and_all_reduce():
+    """TorchExchange.exchange (grouped P2P, one message per key and peer, own
+    block by reference) and all_reduce on gloo, world size 2."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}
+
+
+def test_whole_scale_owners_balance():
+    from paper_1211_1680_b200 import distributed as D
+
+    bands = [2, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 4096]   # C5
+    own = D.whole_scale_owners(bands, 8)
+    assert sorted(own) == [j for j, k in enumerate(bands) if k <= 256]
+    assert own[8] != own[7]                 # the two largest whole scales apart
+    assert D.whole_scale_owners(bands, 1) == {j: 0 for j in own}
+    assert D.whole_scale_owners([27, 27, 81, 243, 729, 2048, 2048], 4, whole_max=0) == {}

@@ -23,33 +23,78 @@ def env():
     return torch, sw, D, WaveletTransform
 
 
+def _check_sharded(env, L, P, real, scheme, lam=2.0, j0=1, batch=1, whole_max=256, tol=1e-12,
+                   multires=True):
+    torch, sw, D, WT = env
+    sch = getattr(sw.SamplingScheme, scheme)
+    cfg = sw.TransformConfig(L, lam, j0, scheme=sch, multires=multires)
+    rng = np.random.default_rng(P + 10 * real + L)
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform
+
+    sht = SphericalHarmonicTransform(sch, L)
+    f = np.stack([sw.gaussian_coeffs(L, rng, real_signal=real).coeffs for _ in range(batch)])
+    x = sht.synthesis(torch.from_numpy(f).cuda(), real=real)
+    ref = WT(cfg, batch=batch, real=real)
+    ref_maps = ref.analysis(x)
+    ex = D.VirtualExchange(P)
+    sh = D.ShardedWaveletTransform(cfg, ex, batch=batch, real=real, whole_max=whole_max)
+    rows = {r: x[:, slice(*sh.ring_block(L, r)), :].contiguous() for r in range(P)}
+    out = sh.analysis(rows)
+    for j, k in enumerate(sh.bands):
+        if j in sh.whole_owner:
+            o = sh.whole_owner[j]
+            full = out[o][j]
+            assert all(out[r][j].shape[1] == 0 for r in range(P) if r != o)
+        else:
+            full = torch.cat([out[r][j] for r in range(P)], dim=1)
+        err = (full - ref_maps[j]).abs().max().item() / max(ref_maps[j].abs().max().item(), 1e-300)
+        assert err <= tol, (j, err)
+    back = sh.synthesis(out)
+    y = torch.cat([back[r] for r in range(P)], dim=1)
+    assert (y - x).abs().max().item() <= 1e-10 * x.abs().max().item()
+    return sh
+
+
 @pytest.mark.parametrize("P", [1, 2, 3])
 @pytest.mark.parametrize("real", [False, True])
 @pytest.mark.parametrize("scheme", ["MW", "GL"])
 def test_sharded_matches_unsharded(env, P, real, scheme):
+    sh = _check_sharded(env, 96, P, real, scheme, whole_max=16)
+    assert sh.whole_owner and sh.large      # both placements exercised
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_all_large_and_all_whole(env, P):
+    sh = _check_sharded(env, 64, P, False, "MW", whole_max=0)
+    assert not sh.whole_owner
+    # full resolution: every scale on the top grid (5 sets on one grid: chunked launches)
     torch, sw, D, WT = env
-    L = 96
-    sch = getattr(sw.SamplingScheme, scheme)
-    cfg = sw.TransformConfig(L, 2.0, 1, scheme=sch, multires=True)
-    rng = np.random.default_rng(P + 10 * real)
-    f = sw.gaussian_coeffs(L, rng, real_signal=real)
-    x = torch.from_numpy(sw.sh_synthesis(f, sw.make_grid(sch, L)).values.copy()).cuda()
-    if real:
-        x = x.real.contiguous()
-    x = x[None]
-    ref = WT(cfg, batch=1, real=real)
-    ref_maps = ref.analysis(x)
-    ex = D.VirtualExchange(P)
-    sh = D.ShardedWaveletTransform(cfg, ex, batch=1, real=real)
-    rows = {r: x[:, slice(*sh.ring_block(L, r)), :].contiguous() for r in range(P)}
-    out = sh.analysis(rows)
-    for j, k in enumerate(sh.bands):
-        full = torch.cat([out[r][j] for r in range(P)], dim=1)
-        err = (full - ref_maps[j]).abs().max().item() / max(ref_maps[j].abs().max().item(), 1e-300)
-        assert err <= 1e-12, (j, err)
-    back = sh.synthesis(out)
-    y = torch.cat([back[r] for r in range(P)], dim=1)
-    assert (y - x).abs().max().item() <= 1e-10 * x.abs().max().item()
+    sh = _check_sharded(env, 48, P, True, "GL", whole_max=0, lam=2.0, j0=0, multires=False)
+    assert list(sh.large_groups) == [48] and len(sh.large_groups[48]) > 3
+    sh = _check_sharded(env, 64, P, True, "MW", whole_max=64)
+    assert not sh.large
+
+
+@pytest.mark.parametrize("L,real", [(1024, False), (1024, True), (2048, False), (2048, True)])
+def test_sharded_at_large_bands(env, L, real):
+    """The MW synthesis resampling (k >= 1024) and the k2 prime-factor / theta
+    kernels with a rank's subset of orders (ADVICE: untested at L = 96)."""
+    _check_sharded(env, L, 2, real, "MW", lam=3.0 if L == 2048 else 2.0,
+                   j0=2 if L == 2048 else 3, tol=1e-11)
+
+
+def test_sharded_batch_two(env):
+    _check_sharded(env, 96, 2, False, "MW", batch=2, whole_max=16)
+
+
+def test_exchange_bytes(env):
+    _, sw, D, _ = env
+    cfg = sw.TransformConfig(2048, 3.0, 2, scheme=sw.SamplingScheme.MW, multires=True)
+    sh = D.ShardedWaveletTransform(cfg, D.VirtualExchange(2), batch=1, real=False)
+    b = sh.exchange_bytes()
+    # top all-to-all: half the rings x half the bins x 16 B leave each rank
+    assert 0.4 * 2048 * 4095 * 16 / 2 < b["top_a2a"] < 0.6 * 2048 * 4095 * 16
+    assert b["whole_allreduce"] == 243 * 243 * 16
 
 
 def test_partition_covers_everything(env):
