@@ -473,7 +473,8 @@ def workload_config(cfgname, bands, mode, ws, map_bytes):
                     f"{'multires' if cfg['multires'] else 'full-res'}",
         "L": L, "batch": B, "bands": [int(b) for b in bands],
         "parallelism": {"single": "single GPU", "replica": f"replicas x{ws}",
-                        "shard": f"orders/rings sharded x{ws} (NCCL all-to-all)"}[mode],
+                        "shard": f"orders/rings sharded x{ws} (NCCL grouped P2P exchange; "
+                                 "scales <= 256 whole on one rank)"}[mode],
         "l2": f"inputs larger than L2 (map {map_bytes / 1e6:.0f} MB, working set > 1 GB)"
               if L >= 1024 else "small config (L2-resident)",
     }

@@ -284,6 +284,7 @@ class ShardedWaveletTransform:
         _device.require_cuda()
         self.cfg, self.ex, self.B, self.real = config, exchange, batch, bool(real)
         self.P = exchange.P
+        self.whole_max = whole_max
         kern = kernels_for(config)
         self.bands = scale_bands(config, kern)
         L = config.L
@@ -547,19 +548,28 @@ class ShardedWaveletTransform:
         return ring_blocks(k, self.P)[rank]
 
     def exchange_bytes(self) -> dict:
-        """Bytes that leave each rank per exchange of one round trip (the
-        all-to-alls move G / H blocks of complex128; own blocks stay local)."""
-        L, B = self.cfg.L, self.B
+        return exchange_bytes(self.cfg, self.P, self.B, self.real, self.whole_max)
 
-        def a2a(k):
-            g = ring_blocks(k, self.P)
-            orders = [np.nonzero(self.owner[:k] == r)[0] for r in range(self.P)]
-            nb = [len(shard_bins(k, o, self.real)) for o in orders]
-            per = [sum(B * nb[q] * (g[r][1] - g[r][0]) * 16 for q in range(self.P) if q != r)
-                   for r in range(self.P)]
-            return max(per)
 
-        large = sum(a2a(self.bands[j]) for j in self.large)
-        ar = B * self.ks * self.ks * 16
-        return {"top_a2a": a2a(L), "large_scales_a2a": large, "whole_allreduce": ar,
-                "per_round_trip_max_rank": 2 * a2a(L) + 2 * large + 2 * ar}
+def exchange_bytes(config: TransformConfig, P: int, batch: int = 1, real: bool = False,
+                   whole_max: int = 256) -> dict:
+    """Bytes that leave the busiest rank per exchange of one round trip (pure
+    host arithmetic): the exchanges move G / H blocks of complex128, a rank's
+    own block stays local; the all-reduces move B k_s^2 complex128."""
+    L, B = config.L, batch
+    bands = scale_bands(config, kernels_for(config))
+    owner = order_owner(L, P)
+    whole = whole_scale_owners(bands, P, whole_max)
+    ks = max([bands[j] for j in whole], default=0)
+
+    def a2a(k):
+        g = ring_blocks(k, P)
+        orders = [np.nonzero(owner[:k] == r)[0] for r in range(P)]
+        nb = [len(shard_bins(k, o, real)) for o in orders]
+        return max(sum(B * nb[q] * (g[r][1] - g[r][0]) * 16 for q in range(P) if q != r)
+                   for r in range(P))
+
+    large = sum(a2a(k) for j, k in enumerate(bands) if j not in whole)
+    ar = B * ks * ks * 16
+    return {"top_a2a": a2a(L), "large_scales_a2a": large, "whole_allreduce": ar,
+            "per_round_trip_max_rank": 2 * a2a(L) + 2 * large + 2 * ar}
