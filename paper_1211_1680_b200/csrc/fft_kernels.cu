@@ -26,6 +26,14 @@
 
 namespace s2w {
 
+// 32-byte store (STG.E.256 on sm_100a): one full sector.  p must be 32-byte aligned.
+S2W_DEV void st_global_32(double2* p, double2 lo, double2 hi) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(lo.x), "d"(lo.y), "d"(hi.x),
+               "d"(hi.y)
+               : "memory");
+}
+S2W_DEV bool aligned32(const void* p) { return ((uintptr_t)p & 31) == 0; }
+
 // resident CTAs per SM the row kernels are compiled for (register cap):
 // two for the 4096-point rows (k = 729 .. 1024 class grids), else one
 #ifndef S2W_ROW_MINB12
@@ -211,8 +219,13 @@ __global__ void __launch_bounds__(PFA_T) phi_fwd_pfa_kernel(PhiFwdArgs a) {
     } else {
       const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
       const double h = 0.5 * a.scale;
-      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
-      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      const double2 r0 = cscale(cadd(z, zr), h), r1 = cscale(cmul_mi(csub(z, zr)), h);
+      double2* o = fwd_row(a, set, mi) + ta;
+      if (vb && aligned32(o)) st_global_32(o, r0, r1);  // the ring pair: one sector
+      else {
+        o[0] = r0;
+        if (vb) o[1] = r1;
+      }
     }
   }
 }
@@ -431,8 +444,20 @@ S2W_DEV ThetaSynRow theta_syn_row(const ThetaSynArgs& a, int row, bool valid) {
 
 S2W_DEV void theta_syn_store(const ThetaSynRow& R, const ThetaSynArgs& a, int t, double2 wt,
                              double2 wr) {
-  if (R.ce >= 0) R.out[(size_t)t * a.n_bins + R.ce] = cscale(cadd(wt, wr), 0.5);
-  if (R.co >= 0) R.out[(size_t)t * a.n_bins + R.co] = cscale(csub(wt, wr), 0.5);
+  const double2 ve = cscale(cadd(wt, wr), 0.5), vo = cscale(csub(wt, wr), 0.5);
+  double2* row = R.out + (size_t)t * a.n_bins;
+  // the pair's columns are adjacent bins (theta_pairs): one 32-byte store
+  // (a full sector) where the row alignment allows it
+  if (R.ce >= 0 && R.co == R.ce + 1 && ((uintptr_t)(row + R.ce) & 31) == 0) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(row + R.ce), "d"(ve.x),
+                 "d"(ve.y), "d"(vo.x), "d"(vo.y) : "memory");
+  } else if (R.co >= 0 && R.ce == R.co + 1 && ((uintptr_t)(row + R.co) & 31) == 0) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(row + R.co), "d"(vo.x),
+                 "d"(vo.y), "d"(ve.x), "d"(ve.y) : "memory");
+  } else {
+    if (R.ce >= 0) row[R.ce] = ve;
+    if (R.co >= 0) row[R.co] = vo;
+  }
 }
 
 // PFA: N = 4095, the inverse DFT_N of step 4 runs on the prime-factor engine.
@@ -851,6 +876,7 @@ constexpr int K2_TT = S2W_K2_TT;  // theta_k2 threads
 #define S2W_K2_PHI_MINB 2
 #endif
 
+
 template <int T>
 __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB) phi_fwd_k2_kernel(PhiFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
@@ -907,11 +933,17 @@ __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB) phi_fwd_k2_kernel(PhiFwdAr
     } else {
       const double2 zr = cconj(buf[pfa_pos(mi ? N - mi : 0)]);
       const double h = 0.5 * a.scale;
-      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
-      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      const double2 r0 = cscale(cadd(z, zr), h), r1 = cscale(cmul_mi(csub(z, zr)), h);
+      double2* o = fwd_row(a, set, mi) + ta;
+      if (vb && aligned32(o)) st_global_32(o, r0, r1);  // the ring pair: one sector
+      else {
+        o[0] = r0;
+        if (vb) o[1] = r1;
+      }
     }
   }
 }
+
 
 template <int T>
 __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB + 1) phi_inv_k2_kernel(PhiInvArgs a) {
@@ -1123,8 +1155,13 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
     } else {
       const double2 zr = cconj(rader_bin<false>(buf, R, x0, X0, mi ? N - mi : 0));
       const double h = 0.5 * a.scale;
-      fwd_row(a, set, mi)[ta] = cscale(cadd(z, zr), h);
-      if (vb) fwd_row(a, set, mi)[ta + 1] = cscale(cmul_mi(csub(z, zr)), h);
+      const double2 r0 = cscale(cadd(z, zr), h), r1 = cscale(cmul_mi(csub(z, zr)), h);
+      double2* o = fwd_row(a, set, mi) + ta;
+      if (vb && aligned32(o)) st_global_32(o, r0, r1);  // the ring pair: one sector
+      else {
+        o[0] = r0;
+        if (vb) o[1] = r1;
+      }
     }
   }
 }
