@@ -45,6 +45,21 @@ CONFIGS = {
 }
 
 
+def _executed(cfgname, kernel, mode):
+    """Executed FP64 (+ DMMA) pipe utilisation of the roofline stage from the
+    committed ncu capture (profiles/roofline_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "roofline_traffic.json")
+    if mode == "shard" or not os.path.exists(path):
+        return None, None
+    try:
+        with open(path) as fh:
+            rec = json.load(fh).get(cfgname, {}).get(kernel)
+        return (float(rec["executed_pipe_frac"]), rec.get("executed_note")) if rec else (None, None)
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def _traffic(cfgname, kernel, mode):
     """DRAM bytes per launch of the roofline kernel from the committed ncu capture
     (profiles/roofline_traffic.json), or None when none matches this workload."""
@@ -397,6 +412,10 @@ def run_ours(args, cfgname):
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if achieved else None,
             "traffic": _traffic(cfgname, dom, mode),
+            # canonical FLOPs count the unsymmetrised work; the kernels execute about
+            # half of it (equator symmetry), so the hardware view is the pipe utilisation
+            "executed_frac": _executed(cfgname, dom, mode)[0],
+            "executed_note": _executed(cfgname, dom, mode)[1],
             "traffic_unit": "bytes per launch (DRAM read + write, ncu --set full)",
             "flops_per_rt": fl[dom] * shard_frac,
             "stage_ms_per_rt": dms / n_prof,
