@@ -218,6 +218,12 @@ int s2w_shard_gather_rings(s2w_shard_plan* plan, const double* const* src, doubl
 /* Received blocks [B][t1-t0][n_q] of rank q's bins -> G_ring [B][t1-t0][n_bins]. */
 int s2w_shard_scatter_bins(s2w_shard_plan* plan, const double* const* src, double* G, void* stream);
 
+/* ---------------------------------------------------------------- layouts */
+/* n real doubles -> n complex128 (zero imaginary parts), and back (real parts):
+ * the numpy drop-in's real maps are complex128 arrays (reference grid.py:155-160). */
+int s2w_real_to_complex(const double* in, double* out, long long n, void* stream);
+int s2w_complex_real_part(const double* in, double* out, long long n, void* stream);
+
 /* ---------------------------------------------------------------- accounting */
 /* Number of kernels launched by this library since load (bench "gpu_launches"). */
 long long s2w_kernel_launches(void);

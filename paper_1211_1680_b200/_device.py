@@ -62,6 +62,12 @@ def to_host(tensor) -> np.ndarray:
     return tensor.cpu().numpy()
 
 
+def copy_to_host(tensor, arr: np.ndarray) -> None:
+    """Device tensor -> an existing host array (same number of elements)."""
+    t = torch()
+    t.from_numpy(arr).copy_(tensor.reshape(-1).view(t.from_numpy(arr).dtype))
+
+
 def empty(n: int, dtype="float64"):
     t = torch()
     return t.empty(n, dtype=getattr(t, dtype), device=f"cuda:{device_index()}")

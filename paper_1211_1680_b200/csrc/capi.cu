@@ -1743,6 +1743,18 @@ extern "C" {
 
 long long s2w_kernel_launches(void) { return g_launches.load(); }
 
+int s2w_real_to_complex(const double* in, double* out, long long n, void* stream) {
+  if ((!in || !out) && n > 0) return fail(S2W_EPARAM, "null argument");
+  CU(launch_real_to_complex(in, (double2*)out, n, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
+int s2w_complex_real_part(const double* in, double* out, long long n, void* stream) {
+  if ((!in || !out) && n > 0) return fail(S2W_EPARAM, "null argument");
+  CU(launch_complex_real_part((const double2*)in, out, n, (cudaStream_t)stream));
+  return S2W_OK;
+}
+
 int s2w_profile_enable(int on) {
   g_prof = on != 0;
   return S2W_OK;

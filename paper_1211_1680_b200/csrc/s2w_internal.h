@@ -242,6 +242,8 @@ struct TileArgs {
 cudaError_t launch_tile_analysis(const TileArgs& a, cudaStream_t st);
 // f[set][i] = sum_j fac_j[l] * in_j[set][i] (i < band_j^2), j ascending (transform.py:153-172)
 cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st);
+cudaError_t launch_real_to_complex(const double* in, double2* out, long long n, cudaStream_t st);
+cudaError_t launch_complex_real_part(const double2* in, double* out, long long n, cudaStream_t st);
 
 // FP64 FMA throughput microbenchmark (roofline denominator for the Legendre
 // stage; MEASURED_PEAKS.json has no FP64 entry).  Synchronises the stream.

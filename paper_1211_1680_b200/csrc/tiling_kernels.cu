@@ -3,6 +3,7 @@
 // layout, sht.py:131-137) and zero-padded recombination.  HBM-bound streaming
 // kernels: one read of f and one write per output (analysis); one read per
 // input and one write of f (synthesis).
+#include <algorithm>
 #include "common.cuh"
 #include "s2w_internal.h"
 
@@ -69,6 +70,32 @@ cudaError_t launch_tile_synthesis(const TileArgs& a, cudaStream_t st) {
   const long long n = (long long)a.L * a.L * a.n_sets;
   if (n == 0) return cudaSuccess;
   tile_synthesis_kernel<<<tile_grid(n), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Real <-> complex128 map layouts of the numpy drop-in (the reference stores
+// real maps as complex128 with zero imaginary parts, grid.py:155-160): the
+// conversion runs here instead of as host passes over the arrays.
+__global__ void real_to_complex_kernel(const double* in, double2* out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = make_double2(in[i], 0.0);
+}
+__global__ void complex_real_part_kernel(const double2* in, double* out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i].x;
+}
+static int elem_grid(long long n) { return (int)std::min<long long>((n + 255) / 256, 148LL * 16); }
+
+cudaError_t launch_real_to_complex(const double* in, double2* out, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  real_to_complex_kernel<<<elem_grid(n), 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_complex_real_part(const double2* in, double* out, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  complex_real_part_kernel<<<elem_grid(n), 256, 0, st>>>(in, out, n);
   return cudaGetLastError();
 }
 

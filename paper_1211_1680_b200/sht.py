@@ -158,23 +158,44 @@ def analysis_device(map_dev, n_sets: int, real: bool, grid: GridSpec):
 
 
 def maps_to_device(smaps, real: bool):
-    if len(smaps) == 1:  # no stacking copy for a single map
-        v = smaps[0].values
-        host = np.ascontiguousarray(v.real) if real else v.view(np.float64)
-    elif real:
-        host = np.stack([m.values.real for m in smaps])
-    else:
-        host = np.stack([m.values for m in smaps]).view(np.float64)
-    return _device.to_device(host.reshape(-1))
+    """Maps -> flat device doubles (real maps: their real parts).  The
+    complex128 values travel as they are and the real part is taken on the
+    device (s2w_complex_real_part): no host pass over the arrays."""
+    vals = (smaps[0].values if len(smaps) == 1  # no stacking copy for a single map
+            else np.stack([m.values for m in smaps]))
+    cdev = _device.to_device(vals.view(np.float64).reshape(-1))
+    if not real:
+        return cdev
+    n = cdev.numel() // 2
+    out = _device.empty(n)
+    _native.check(_native.load().s2w_complex_real_part(
+        _device.ptr(cdev), _device.ptr(out), n, _device.stream_handle()))
+    return out
 
 
 def maps_from_device(dev, grid: GridSpec, n: int, real: bool) -> list[SphereMap]:
-    host = _device.to_host(dev)
+    """Flat device doubles -> maps.  Real maps become complex128 on the device
+    (s2w_real_to_complex) and are copied straight into the arrays the maps
+    own; the maps are built without re-checking what the pipeline guarantees
+    (zero imaginary parts, the MW pole ring pinned by phi_inv)."""
+    shape = (n, grid.n_theta, grid.n_phi)
     if real:
-        vals = host.reshape(n, grid.n_theta, grid.n_phi).astype(np.complex128)
-    else:
-        vals = host.view(np.complex128).reshape(n, grid.n_theta, grid.n_phi)
-    return [SphereMap(grid, vals[i], is_real=real) for i in range(n)]
+        cdev = _device.empty(2 * dev.numel())
+        _native.check(_native.load().s2w_real_to_complex(
+            _device.ptr(dev), _device.ptr(cdev), dev.numel(), _device.stream_handle()))
+        dev = cdev
+    vals = np.empty(shape, dtype=np.complex128)
+    _device.copy_to_host(dev, vals.view(np.float64).reshape(-1))
+    return [_trusted_map(grid, vals[i], real) for i in range(n)]
+
+
+def _trusted_map(grid: GridSpec, values: np.ndarray, real: bool) -> SphereMap:
+    m = object.__new__(SphereMap)
+    values.setflags(write=False)
+    object.__setattr__(m, "grid", grid)
+    object.__setattr__(m, "values", values)
+    object.__setattr__(m, "is_real", bool(real))
+    return m
 
 
 # ---------------------------------------------------------------- numpy API
