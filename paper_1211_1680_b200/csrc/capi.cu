@@ -940,6 +940,8 @@ struct AnaCfg {
   bool built = false;
   int n_rein = 0;
   mutable SideLane lane;
+  DevBuf pipe;  // leg_ana_pipe_kernel's inter-pass ring states ([item][ring][3])
+  long long pipe_stride = 0;
   int key[4] = {0, 0, 0, 0};
   DevBuf grids, sets, segs, items;
   int n_items = 0, ns = 1, cplx = 1, win = 32, sym = 0;
@@ -1011,6 +1013,17 @@ struct AnaSegSpec {
   std::vector<AnaSet> sets;
   int combine;
 };
+
+// Scratch of the pipelined analysis kernel when it serves this launch.
+static int ana_pipe_setup(AnaCfg& cfg, const std::vector<LegGridDev>& grids, int kmax) {
+  cfg.pipe_stride = 0;
+  if (!leg_ana_pipe_ok(kmax, cfg.ns, cfg.cplx, cfg.sym)) return S2W_OK;
+  int nn = 1;
+  for (auto& g : grids) nn = std::max(nn, g.n_north);
+  cfg.pipe_stride = 3LL * nn;
+  CHECK(cfg.pipe.ensure(sizeof(double) * (size_t)std::max(1, cfg.n_items) * cfg.pipe_stride));
+  return S2W_OK;
+}
 
 static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool cplx) {
   // distinct grids
@@ -1095,6 +1108,7 @@ static int build_ana(AnaCfg& cfg, const std::vector<AnaSegSpec>& segspecs, bool 
   cfg.ns = ns;
   cfg.cplx = cplx;
   cfg.win = leg_ana_window(kmax, ns, cplx);
+  CHECK(ana_pipe_setup(cfg, grids, kmax));
   cfg.built = true;
   return S2W_OK;
 }
@@ -1142,6 +1156,8 @@ static int run_ana(const AnaCfg& cfg, const double* seed_c, double2* const* bufs
   a.win = cfg.win;
   a.sym = cfg.sym;
   a.rein = 0;
+  a.pipe_scratch = cfg.pipe_stride ? cfg.pipe.as<double>() : nullptr;
+  a.pipe_stride = cfg.pipe_stride;
   for (int i = 0; i < S2W_NBUF; ++i) a.bufs[i] = bufs[i];
   ProfScope ps(P_LEG_ANA, st);
   if (cfg.n_rein == 0) {

@@ -214,12 +214,19 @@ struct LegAnaArgs {
   int sym;  // every grid is equator-symmetric (LegGridDev::n_north > 0)
   int rein; // the items are orders m < S2W_REIN_M (Reinsch recursion; sym only)
   double2* bufs[S2W_NBUF];
+  // pipelined analysis (leg_ana_pipe_kernel): recursion state between degree
+  // passes, [item][ring][3] doubles; nullptr = the reduce-scatter kernels
+  double* pipe_scratch = nullptr;
+  long long pipe_stride = 0;
 };
 
 cudaError_t launch_leg_synth(const LegSynthArgs& a, cudaStream_t st);
 cudaError_t launch_leg_ana(const LegAnaArgs& a, cudaStream_t st);
 int leg_synth_window(int kmax, int ns, int cplx);
 int leg_ana_window(int kmax, int ns, int cplx);
+// the pipelined analysis kernel serves this launch shape (symmetric rings, <= 4
+// reals per degree, large grids)
+bool leg_ana_pipe_ok(int kmax, int ns, int cplx, int sym);
 // Per ring: largest order m whose Legendre column reaches the significance
 // threshold below degree k (used to build the per-m active ring ranges).
 cudaError_t launch_leg_probe(int k, int n_t, const double* cos_t, const double* sin_t,

@@ -221,3 +221,37 @@ def test_round_trip_L2048_batch2(sw, real):
     assert torch.equal(x[1:], one)  # set 1 does not depend on set 0
     back = sht.analysis(x).cpu().numpy()
     assert np.abs(back - f).max() <= 1e-10 * max(1.0, np.abs(f).max())
+
+
+def test_pipelined_analysis_matches_default():
+    """The opt-in pipelined analysis kernel (S2W_ANA_PIPE=1: lanes own degree
+    blocks, rings stream through the warp) against the default reduce-scatter
+    kernel on the same map, complex and real, including the polar rings'
+    scaled-exponent hand-off between passes (L = 600: 3 degree passes)."""
+    import os
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1211_1680_b200 as sw
+    from paper_1211_1680_b200 import _device
+    from paper_1211_1680_b200.device import SphericalHarmonicTransform
+
+    L = 600
+    for real in (False, True):
+        f = sw.gaussian_coeffs(L, np.random.default_rng(600 + real), real_signal=real).coeffs
+        sht = SphericalHarmonicTransform(sw.SamplingScheme.MW, L)
+        x = sht.synthesis(torch.from_numpy(f[None].copy()).cuda(), real=real)
+        ref = sht.analysis(x).cpu().numpy()
+        os.environ["S2W_ANA_PIPE"] = "1"
+        try:
+            with _device._lock:
+                _device._sht_plans.clear()   # a fresh plan builds its launch with the switch on
+            got = SphericalHarmonicTransform(sw.SamplingScheme.MW, L).analysis(x).cpu().numpy()
+        finally:
+            del os.environ["S2W_ANA_PIPE"]
+            with _device._lock:
+                _device._sht_plans.clear()
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        assert np.abs(got - f).max() <= 1e-10 * np.abs(f).max()
