@@ -195,8 +195,9 @@ class WaveletTransform:
                     self.alloc_scale_maps())
             self._stream_bufs = bufs
         xin, xout, scale = bufs
-        # small maps are launch-bound: replay the transforms from CUDA graphs
-        use_graph = self.config.L <= 512
+        # replay the transforms from CUDA graphs (small maps are launch-bound;
+        # large ones lose the GPU-side gaps between dependent launches)
+        use_graph = True
         if use_graph:
             for b in range(2):
                 self.round_trip_graph(xin[b], scale, xout[b])  # capture outside the pipeline
