@@ -195,9 +195,9 @@ class WaveletTransform:
                     self.alloc_scale_maps())
             self._stream_bufs = bufs
         xin, xout, scale = bufs
-        # replay the transforms from CUDA graphs (small maps are launch-bound;
-        # large ones lose the GPU-side gaps between dependent launches)
-        use_graph = True
+        # small maps are launch-bound: replay the transforms from CUDA graphs
+        # (at L = 2048 graph replays slowed this overlapped stream: 82 vs 91 rt/s)
+        use_graph = self.config.L <= 512
         if use_graph:
             for b in range(2):
                 self.round_trip_graph(xin[b], scale, xout[b])  # capture outside the pipeline
