@@ -238,7 +238,17 @@ def run_ours(args, cfgname):
     st = torch.cuda.current_stream()
 
     if mode == "shard":
-        sh = D.ShardedWaveletTransform(tcfg, D.TorchExchange(), batch=B, real=real)
+        ex = D.TorchExchange()
+        if args.exchange == "peer":
+            # fused exchange over NVLink peer memory (CUDA IPC between the ranks);
+            # a rank set that cannot map its peers' buffers keeps the NCCL path
+            try:
+                ex = D.TorchPeerExchange()
+                ex.alloc_shared(("probe",), {q: (1,) for q in range(ws)}, torch.float64)
+            except Exception as e:  # pragma: no cover - hardware dependent
+                print(f"peer exchange unavailable ({e}); using NCCL P2P", file=sys.stderr)
+                ex = D.TorchExchange()
+        sh = D.ShardedWaveletTransform(tcfg, ex, batch=B, real=real)
         t0, t1 = sh.ring_block(L, rank)
         x = x_full[:, t0:t1, :].contiguous()
         bands = sh.bands
@@ -526,8 +536,8 @@ def workload_config(cfgname, bands, mode, ws, map_bytes):
                     f"{'multires' if cfg['multires'] else 'full-res'}",
         "L": L, "batch": B, "bands": [int(b) for b in bands],
         "parallelism": {"single": "single GPU", "replica": f"replicas x{ws}",
-                        "shard": f"orders/rings sharded x{ws} (NCCL grouped P2P exchange; "
-                                 "scales <= 256 whole on one rank)"}[mode],
+                        "shard": f"orders/rings sharded x{ws} (fused exchange over peer memory or "
+                                 "NCCL P2P; scales <= 256 whole on one rank)"}[mode],
         "l2": f"inputs larger than L2 (map {map_bytes / 1e6:.0f} MB, working set > 1 GB)"
               if L >= 1024 else "small config (L2-resident)",
     }
@@ -625,15 +635,22 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the round trip from a CUDA graph (auto: on, single/replica mode)")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="shard mode: fused exchange over peer memory (kernels store into the "
+                         "owners' buffers) or grouped NCCL P2P messages")
     ap.add_argument("--mode", choices=["single", "shard", "replica"], default=None,
                     help="N=1: single; N>1 default shard (one map split by orders/rings, "
                          "strong scaling) or replica (independent maps, weak scaling)")
     args = ap.parse_args()
+    # stdout carries exactly one JSON line: everything else written to fd 1 by
+    # libraries (NCCL's version banner, torch) goes to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     rec = run_reference(args, args.config) if args.impl == "reference" else run_ours(args, args.config)
     if rec is not None:
-        print(json.dumps(rec), flush=True)
+        print(json.dumps(rec), file=json_out, flush=True)
 
 
 if __name__ == "__main__":

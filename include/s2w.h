@@ -212,6 +212,16 @@ int s2w_shard_legendre_analysis_sets(s2w_shard_plan* plan, int n, const double* 
  * all-to-all packing of distributed.py (round 1). */
 int s2w_shard_set_peers(s2w_shard_plan* plan, int P, int rank, const int* ring_t0t1,
                         const int* n_bins, const int* bins);
+/* Fused exchange over peer memory (NVLink / CUDA IPC pointers, HOST array of P
+ * device pointers, peer_*[q] = rank q's buffer).  rings_forward_peers: the
+ * forward ring DFTs of my rings store each bin row straight into its owner's
+ * H_local [B][n_q][L] (my ring columns), no send buffer and no gather.
+ * push_rings: my G_local [B][L][n_local] (Legendre synthesis output) is
+ * stored straight into every ring owner's G_ring [B][t_q][n_bins].  The
+ * caller orders them against the peers' readers (a barrier before and after). */
+int s2w_shard_rings_forward_peers(s2w_shard_plan* plan, const double* map_rows,
+                                  double* const* peer_H, void* stream);
+int s2w_shard_push_rings(s2w_shard_plan* plan, const double* G, double* const* peer_G, void* stream);
 /* Received blocks [B][n_local][t_q] (src[q], device pointers, HOST array of P)
  * -> H_local [B][n_local][L]. */
 int s2w_shard_gather_rings(s2w_shard_plan* plan, const double* const* src, double* H, void* stream);

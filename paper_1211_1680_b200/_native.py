@@ -72,6 +72,8 @@ _PROTOS = {
     "s2w_shard_set_peers": (_c_int, [_vp, _c_int, _c_int, ctypes.POINTER(_c_int),
                                      ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)]),
     "s2w_shard_gather_rings": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "s2w_shard_rings_forward_peers": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
+    "s2w_shard_push_rings": (_c_int, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "s2w_shard_scatter_bins": (_c_int, [_vp, ctypes.POINTER(_vp), _vp, _vp]),
     "s2w_real_to_complex": (_c_int, [_vp, _vp, ctypes.c_longlong, _vp]),
     "s2w_complex_real_part": (_c_int, [_vp, _vp, ctypes.c_longlong, _vp]),

@@ -61,12 +61,18 @@ struct PhiFwdArgs {
   // plans write each destination rank's bins as one contiguous block
   // (s2w_shard_set_peers); nullptr = [set][mi][ring]
   const long long* ofs = nullptr;
+  // fused exchange (s2w_shard_rings_forward_peers): row (set, bin) goes to
+  // rank peer_q[.]'s buffer peer[q] at offset ofs[.] -- the destination's own
+  // H_local layout, written over peer (NVLink / IPC) pointers
+  const int* peer_q = nullptr;
+  double2* peer[16] = {};
 };
 
 // start of the output row of (set, bin mi) of a forward ring-DFT launch
 __device__ __forceinline__ double2* fwd_row(const PhiFwdArgs& a, int set, int mi) {
-  return a.ofs ? a.out + a.ofs[(size_t)set * a.n_bins + mi]
-               : a.out + ((size_t)set * a.n_bins + mi) * a.n_rings;
+  const size_t i = (size_t)set * a.n_bins + mi;
+  if (a.peer_q) return a.peer[a.peer_q[i]] + a.ofs[i];
+  return a.ofs ? a.out + a.ofs[i] : a.out + i * a.n_rings;
 }
 
 struct PhiInvArgs {
@@ -259,7 +265,7 @@ cudaError_t measure_fp64_peak(double* tflops, cudaStream_t st);
 cudaError_t measure_dmma_peak(double* tflops, cudaStream_t st);
 
 // ------------------------------------------------------------------ shard exchange layouts
-constexpr int S2W_MAX_RANKS = 16;
+constexpr int S2W_MAX_RANKS = 16;  // = the PhiFwdArgs::peer table size
 struct ShardSrc {
   const double2* p[S2W_MAX_RANKS];  // received block per source rank
 };
@@ -271,5 +277,13 @@ cudaError_t launch_shard_gather_rings(const ShardSrc& src, const int2* ring_src,
 // n_src[q] = number of q's bins
 cudaError_t launch_shard_scatter_bins(const ShardSrc& src, const int2* bin_src, const int* n_src,
                                       int B, int t_r, int n_bins, double2* G, cudaStream_t st);
+// push: my G_local [B][k][n_local] -> every ring's owner q, straight into its
+// G_ring [B][t_q][n_bins] at (t - t0_q, bins[i]) over peer pointers
+struct ShardDst {
+  double2* p[S2W_MAX_RANKS];
+};
+cudaError_t launch_shard_push_rings(const double2* G, const ShardDst& dst, const int2* ring_src,
+                                    const int* t_len, const int* bins, int B, int k, int n_local,
+                                    int n_bins, cudaStream_t st);
 
 }  // namespace s2w

@@ -72,4 +72,31 @@ cudaError_t launch_shard_scatter_bins(const ShardSrc& src, const int2* bin_src, 
   return cudaGetLastError();
 }
 
+// Fused synthesis-direction exchange: each element of my G_local goes
+// straight to the owner of its ring, into that rank's G_ring row (a store over
+// NVLink when the owner is another GPU).  Reads coalesced along my bins.
+__global__ void shard_push_rings_kernel(const double2* G, ShardDst dst, const int2* ring_src,
+                                        const int* t_len, const int* bins, int B, int k, int nl,
+                                        int nb) {
+  const long long total = (long long)B * k * nl;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nl);
+    const long long bt = e / nl;  // b * k + t
+    const int t = (int)(bt % k), b = (int)(bt / k);
+    const int2 qs = __ldg(&ring_src[t]);
+    dst.p[qs.x][((long long)b * __ldg(&t_len[qs.x]) + qs.y) * nb + __ldg(&bins[i])] = G[e];
+  }
+}
+
+cudaError_t launch_shard_push_rings(const double2* G, const ShardDst& dst, const int2* ring_src,
+                                    const int* t_len, const int* bins, int B, int k, int n_local,
+                                    int n_bins, cudaStream_t st) {
+  const long long n = (long long)B * k * n_local;
+  if (n == 0) return cudaSuccess;
+  shard_push_rings_kernel<<<grid_for(n), 256, 0, st>>>(G, dst, ring_src, t_len, bins, B, k, n_local,
+                                                        n_bins);
+  return cudaGetLastError();
+}
+
 }  // namespace s2w

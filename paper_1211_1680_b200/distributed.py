@@ -53,6 +53,8 @@ __all__ = [
     "shard_bins",
     "TorchExchange",
     "VirtualExchange",
+    "TorchPeerExchange",
+    "VirtualPeerExchange",
     "ShardedWaveletTransform",
 ]
 
@@ -199,6 +201,78 @@ class VirtualExchange:
 
     def all_to_all(self, sends: dict, recv_sizes: dict = None) -> dict:
         return {r: [sends[q][r].reshape(-1) for q in range(self.P)] for r in self.ranks}
+
+
+class VirtualPeerExchange(VirtualExchange):
+    """Fused exchange over peer memory, P virtual ranks in one process: every
+    rank's receive buffers are plain device tensors, and a rank's kernels store
+    straight into the other ranks' buffers (on one GPU the "peer" pointers are
+    local; the same kernels take NVLink pointers across GPUs)."""
+
+    peer = True
+
+    def __init__(self, P: int):
+        super().__init__(P)
+        self._bufs = {}
+
+    def alloc_shared(self, key, shapes: dict, dtype):
+        """{rank: tensor} receive buffers (persistent per key) and, per writing
+        rank, the table of every rank's buffer pointer."""
+        th = _device.torch()
+        if key not in self._bufs:
+            dev = f"cuda:{_device.device_index()}"
+            bufs = {q: th.empty(shapes[q], dtype=dtype, device=dev) for q in range(self.P)}
+            self._bufs[key] = (bufs, {r: [bufs[q] for q in range(self.P)] for r in self.ranks})
+        return self._bufs[key]
+
+    def barrier(self):
+        pass  # one stream: the writers precede the readers in stream order
+
+
+class TorchPeerExchange(TorchExchange):
+    """Fused exchange over peer memory between processes of one node: each
+    rank allocates its receive buffers, shares them by CUDA IPC handles
+    (all_gather_object) and opens its peers' -- the exchanging kernels then
+    store over NVLink.  barrier(): NCCL all-reduce of a flag, stream-ordered
+    (all ranks' writes complete before any reader starts); on gloo (tests) a
+    host-side synchronize + barrier."""
+
+    peer = True
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        th = _device.torch()
+        self._bufs = {}
+        self._flag = th.zeros(1, device=f"cuda:{_device.device_index()}")
+        self._nccl = self.dist.get_backend(group) == "nccl"
+
+    def alloc_shared(self, key, shapes: dict, dtype):
+        th = _device.torch()
+        if key not in self._bufs:
+            (me,) = self.ranks
+            dev = f"cuda:{_device.device_index()}"
+            mine = th.empty(shapes[me], dtype=dtype, device=dev)
+            if mine.numel() == 0:
+                mine = th.empty(1, dtype=dtype, device=dev)  # a handle even for an empty block
+            handle = mine.untyped_storage()._share_cuda_()
+            handles = [None] * self.P
+            self.dist.all_gather_object(handles, handle, group=self.group)
+            table = []
+            for q in range(self.P):
+                if q == me:
+                    table.append(mine)
+                else:
+                    st = th.UntypedStorage._new_shared_cuda(*handles[q])
+                    table.append(th.empty(0, dtype=dtype, device=dev).set_(st))
+            self._bufs[key] = ({me: mine.view(shapes[me]) if mine.numel() else mine}, {me: table})
+        return self._bufs[key]
+
+    def barrier(self):
+        if self._nccl:
+            self.dist.all_reduce(self._flag, group=self.group)
+        else:
+            _device.torch().cuda.synchronize()
+            self.dist.barrier(group=self.group)
 
 
 # ---------------------------------------------------------------- GPU backend
@@ -348,9 +422,64 @@ class ShardedWaveletTransform:
         th = _device.torch()
         return th.float64 if self.real else th.complex128
 
+    def _forward_peers(self, items: list) -> dict:
+        """Fused analysis-direction exchange: the ring DFTs of every rank store
+        their bins straight into the owners' H_local (s2w_shard_rings_forward_peers)."""
+        th = _device.torch()
+        self.ex.barrier()  # the owners have finished reading their previous H
+        bufs = {}
+        for key, k, plan_of, rows in items:
+            g = self.grids[k]
+            shapes = {q: (self.B, len(g.bins[q]), k) for q in range(self.P)}
+            own, tables = self.ex.alloc_shared(("H", key), shapes, th.complex128)
+            bufs[key] = own
+            for r in self.ex.ranks:
+                plan_of(r).call("s2w_shard_rings_forward_peers", _device.ptr(rows[r]),
+                                _ptrs(tables[r]), self._stream())
+        self.ex.barrier()  # every rank's stores have landed
+        out = {}
+        for r in self.ex.ranks:
+            out[r] = {}
+            for key, k, plan_of, _ in items:
+                H = bufs[key][r]
+                if len(self.grids[k].bins[r]):
+                    plan_of(r).call("s2w_shard_theta", _device.ptr(H), self._stream())
+                out[r][key] = H
+        return out
+
+    def _inverse_peers(self, items: list) -> dict:
+        """Fused synthesis-direction exchange: every rank pushes its G_local
+        straight into the ring owners' G_ring (s2w_shard_push_rings)."""
+        th = _device.torch()
+        self.ex.barrier()  # the owners have finished reading their previous G_ring
+        bufs = {}
+        for key, k, plan_of, gl in items:
+            g = self.grids[k]
+            shapes = {q: (self.B, g.blocks[q][1] - g.blocks[q][0], self._nb(k)) for q in range(self.P)}
+            own, tables = self.ex.alloc_shared(("G", key), shapes, th.complex128)
+            bufs[key] = own
+            for r in self.ex.ranks:
+                plan_of(r).call("s2w_shard_push_rings", _device.ptr(gl[r]), _ptrs(tables[r]),
+                                self._stream())
+        self.ex.barrier()
+        out = {}
+        for r in self.ex.ranks:
+            out[r] = {}
+            for key, k, plan_of, _ in items:
+                g = self.grids[k]
+                t = g.blocks[r][1] - g.blocks[r][0]
+                x = th.empty((self.B, t, 2 * k - 1), dtype=self._map_dtype(), device=self.dev)
+                if t:
+                    plan_of(r).call("s2w_shard_rings_inverse", _device.ptr(bufs[key][r]),
+                                    _device.ptr(x), self._stream())
+                out[r][key] = x
+        return out
+
     def _forward_many(self, items: list) -> dict:
         """items: [(key, k, plan_of(r), {rank: map rows})] -> {rank: {key: H_local}}
         (ring DFTs of my rings, ONE grouped exchange, MW theta stage)."""
+        if getattr(self.ex, "peer", False):
+            return self._forward_peers(items)
         th = _device.torch()
         sends, shapes, gcols = {}, {}, {}
         for r in self.ex.ranks:
@@ -393,6 +522,8 @@ class ShardedWaveletTransform:
     def _inverse_many(self, items: list) -> dict:
         """items: [(key, k, plan_of(r), {rank: G_local [B][k][n_local]})] ->
         {rank: {key: map rows}} (ONE grouped exchange, ring inverse DFTs)."""
+        if getattr(self.ex, "peer", False):
+            return self._inverse_peers(items)
         th = _device.torch()
         sends, shapes = {}, {}
         for r in self.ex.ranks:

@@ -24,7 +24,7 @@ def env():
 
 
 def _check_sharded(env, L, P, real, scheme, lam=2.0, j0=1, batch=1, whole_max=256, tol=1e-12,
-                   multires=True):
+                   multires=True, peer=False):
     torch, sw, D, WT = env
     sch = getattr(sw.SamplingScheme, scheme)
     cfg = sw.TransformConfig(L, lam, j0, scheme=sch, multires=multires)
@@ -36,7 +36,7 @@ def _check_sharded(env, L, P, real, scheme, lam=2.0, j0=1, batch=1, whole_max=25
     x = sht.synthesis(torch.from_numpy(f).cuda(), real=real)
     ref = WT(cfg, batch=batch, real=real)
     ref_maps = ref.analysis(x)
-    ex = D.VirtualExchange(P)
+    ex = D.VirtualPeerExchange(P) if peer else D.VirtualExchange(P)
     sh = D.ShardedWaveletTransform(cfg, ex, batch=batch, real=real, whole_max=whole_max)
     rows = {r: x[:, slice(*sh.ring_block(L, r)), :].contiguous() for r in range(P)}
     out = sh.analysis(rows)
@@ -109,3 +109,87 @@ def test_partition_covers_everything(env):
         blocks = D.ring_blocks(L, P)
         assert blocks[0][0] == 0 and blocks[-1][1] == L
         assert all(b[1] == c[0] for b, c in zip(blocks, blocks[1:]))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("real", [False, True])
+def test_fused_peer_exchange(env, P, real):
+    """The fused exchange (ring-DFT epilogue storing into the owners' H_local,
+    Legendre-synthesis rows pushed into the owners' G_ring) gives the same
+    transform as the unsharded one; twice, so the persistent receive buffers
+    are reused."""
+    _check_sharded(env, 96, P, real, "MW", whole_max=16, peer=True)
+    _check_sharded(env, 96, P, real, "GL", whole_max=16, peer=True)
+
+
+def test_fused_peer_exchange_large(env):
+    _check_sharded(env, 2048, 2, False, "MW", lam=3.0, j0=2, tol=1e-11, peer=True)
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_1211_1680_b200 as sw
+        from paper_1211_1680_b200 import distributed as D
+        from paper_1211_1680_b200.device import SphericalHarmonicTransform, WaveletTransform
+
+        L = 128
+        cfg = sw.TransformConfig(L, 2.0, 1, scheme=sw.SamplingScheme.MW, multires=True)
+        f = sw.gaussian_coeffs(L, np.random.default_rng(7), real_signal=False).coeffs
+        x = SphericalHarmonicTransform(sw.SamplingScheme.MW, L).synthesis(
+            torch.from_numpy(f[None].copy()).cuda())
+        ref = WaveletTransform(cfg, batch=1, real=False).analysis(x)
+        sh = D.ShardedWaveletTransform(cfg, D.TorchPeerExchange(), batch=1, real=False,
+                                       whole_max=16)
+        t0, t1 = sh.ring_block(L, rank)
+        ok = True
+        for _ in range(2):
+            out = sh.analysis({rank: x[:, t0:t1].contiguous()})[rank]
+            for j, k in enumerate(sh.bands):
+                if j in sh.whole_owner:
+                    if sh.whole_owner[j] == rank:
+                        ok &= (out[j] - ref[j]).abs().max().item() <= 1e-12 * ref[j].abs().max().item()
+                else:
+                    a, b = sh.ring_block(k, rank)
+                    ok &= (out[j] - ref[j][:, a:b]).abs().max().item() <= 1e-12 * ref[j].abs().max().item()
+            back = sh.synthesis({rank: out})[rank]
+            ok &= (back - x[:, t0:t1]).abs().max().item() <= 1e-10 * x.abs().max().item()
+        torch.cuda.synchronize()
+        dist.barrier()
+        q.put((rank, bool(ok), None))
+        dist.destroy_process_group()
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, False, repr(e)))
+
+
+def test_fused_peer_exchange_cuda_ipc_two_processes(env):
+    """Two processes on the one GPU: receive buffers shared by CUDA IPC
+    handles (TorchPeerExchange), the exchanging kernels store into the other
+    process's buffers, gloo + device synchronisation as the barrier."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    assert all(ok for _, ok, _ in res), res
