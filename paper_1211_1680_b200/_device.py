@@ -6,6 +6,7 @@ stream; all arithmetic on the hot path happens in libs2w.so kernels.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import warnings
 
@@ -59,13 +60,44 @@ def to_device(arr: np.ndarray):
 
 
 def to_host(tensor) -> np.ndarray:
-    return tensor.cpu().numpy()
+    """Device float64 tensor -> a new flat host float64 array (host_result)."""
+    return host_result(tensor, np.float64)
 
 
 def copy_to_host(tensor, arr: np.ndarray) -> None:
     """Device tensor -> an existing host array (same number of elements)."""
     t = torch()
     t.from_numpy(arr).copy_(tensor.reshape(-1).view(t.from_numpy(arr).dtype))
+
+
+# Result arrays up to this many bytes come from torch's caching pinned-host
+# allocator (S2W_PINNED_RESULT_MB, 0 disables): page-locked memory takes the
+# device->host copy at PCIe rate with no driver staging and no first-touch
+# page faults, and a map handed back to the next call (run_trial's
+# analysis -> synthesis pair, reference bench.py:84-92) goes host->device at
+# PCIe rate too.  The numpy array keeps the tensor (and so the block) alive;
+# when the caller drops it the block returns to torch's pool for the next call.
+_PINNED_CAP = int(float(os.environ.get("S2W_PINNED_RESULT_MB", "2048")) * (1 << 20))
+
+
+def host_result(tensor, dtype) -> np.ndarray:
+    """Device tensor -> a new host array of `dtype` (flat), through a
+    page-locked buffer when it fits the cap, else a pageable numpy array."""
+    t = torch()
+    flat = tensor.reshape(-1)
+    nbytes = flat.numel() * flat.element_size()
+    if 0 < nbytes <= _PINNED_CAP:
+        try:
+            host = t.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+        except RuntimeError:
+            host = None  # pinned pool exhausted: fall through to pageable memory
+        if host is not None:
+            host.copy_(flat, non_blocking=True)
+            t.cuda.current_stream().synchronize()
+            return host.numpy().view(dtype)
+    arr = np.empty(nbytes // np.dtype(dtype).itemsize, dtype=dtype)
+    copy_to_host(flat, arr.view(np.float64) if flat.dtype == t.float64 else arr)
+    return arr
 
 
 def empty(n: int, dtype="float64"):

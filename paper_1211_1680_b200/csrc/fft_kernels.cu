@@ -875,10 +875,16 @@ constexpr int K2_TT = S2W_K2_TT;  // theta_k2 threads
 #ifndef S2W_K2_PHI_MINB
 #define S2W_K2_PHI_MINB 2
 #endif
+#ifndef S2W_K2_TSYN_MINB
+#define S2W_K2_TSYN_MINB 2
+#endif
+#ifndef S2W_K2_PHIF_MINB
+#define S2W_K2_PHIF_MINB S2W_K2_PHI_MINB
+#endif
 
 
 template <int T>
-__global__ void __launch_bounds__(T, S2W_K2_PHI_MINB) phi_fwd_k2_kernel(PhiFwdArgs a) {
+__global__ void __launch_bounds__(T, S2W_K2_PHIF_MINB) phi_fwd_k2_kernel(PhiFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   double2* buf = smem;
   uint64_t* mb = reinterpret_cast<uint64_t*>(smem + K2_M);
@@ -1020,7 +1026,7 @@ __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB + 1) phi_inv_k2_kernel(PhiI
 }
 
 template <int T>
-__global__ void __launch_bounds__(T, 2) theta_syn_k2_kernel(ThetaSynArgs a) {
+__global__ void __launch_bounds__(T, S2W_K2_TSYN_MINB) theta_syn_k2_kernel(ThetaSynArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   double2* buf = smem;           // [4096]
   double2* tw = smem + K2_M;     // [272]

@@ -184,8 +184,7 @@ def maps_from_device(dev, grid: GridSpec, n: int, real: bool) -> list[SphereMap]
         _native.check(_native.load().s2w_real_to_complex(
             _device.ptr(dev), _device.ptr(cdev), dev.numel(), _device.stream_handle()))
         dev = cdev
-    vals = np.empty(shape, dtype=np.complex128)
-    _device.copy_to_host(dev, vals.view(np.float64).reshape(-1))
+    vals = _device.host_result(dev, np.complex128).reshape(shape)
     return [_trusted_map(grid, vals[i], real) for i in range(n)]
 
 

@@ -158,3 +158,33 @@ def test_concurrent_scales_bit_identical(sw, rng, L, real):
         g = wt.round_trip_graph(x, scale, out)
     torch.cuda.synchronize()
     assert torch.equal(g, outs[False][1])
+
+
+def test_results_in_page_locked_arrays(sw, monkeypatch):
+    """Result arrays come from the pinned-host pool (same values as the
+    pageable path, S2W_PINNED_RESULT_MB = 0), outlive the call that made them
+    and are not overwritten by later calls."""
+    import torch
+
+    from paper_1211_1680_b200 import _device
+
+    L = 48
+    rng = np.random.default_rng(7)
+    f = sw.gaussian_coeffs(L, rng, real_signal=False)
+    cfg = sw.TransformConfig(L, 2.0, 1, scheme=sw.SamplingScheme.MW, multires=True)
+    smap = sw.sh_synthesis(f, sw.make_grid(sw.SamplingScheme.MW, L))
+    assert torch.from_numpy(np.asarray(smap.values)).is_pinned()
+    dec = sw.wav_analysis_pixel(smap, cfg)
+    kept = [np.array(m.values) for m in (dec.scaling, *dec.wavelets)]
+    assert all(torch.from_numpy(np.asarray(m.values)).is_pinned() for m in dec.wavelets)
+    # later calls reuse freed blocks only: the maps still held keep their values
+    for _ in range(3):
+        back = sw.wav_synthesis_pixel(sw.wav_analysis_pixel(smap, cfg))
+    for m, k in zip((dec.scaling, *dec.wavelets), kept):
+        assert np.array_equal(m.values, k)
+    assert rel_err(back.values, smap.values) < TOL
+    monkeypatch.setattr(_device, "_PINNED_CAP", 0)
+    dec0 = sw.wav_analysis_pixel(smap, cfg)
+    assert not torch.from_numpy(np.asarray(dec0.scaling.values)).is_pinned()
+    for m, m0 in zip((dec.scaling, *dec.wavelets), (dec0.scaling, *dec0.wavelets)):
+        assert np.array_equal(m.values, m0.values)
