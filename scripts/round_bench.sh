@@ -7,6 +7,7 @@ T=${1:-rX}
 O=gpurun_out
 mkdir -p $O
 timeout 900 python -m pytest tests -q -m gpu -rf > $O/${T}_pytest.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${T}_smoke.log 2>&1
 python bench.py > $O/${T}_bench.json 2> $O/${T}_bench.err
 for c in C1 C2 C3 C5; do
   python bench.py --config $c --no-cpu --steps 10 > $O/${T}_bench_${c,,}.json 2>> $O/${T}_bench.err
@@ -17,4 +18,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${
 ncu --set full --import-source on --clock-control none \
   -k regex:"leg_ana|leg_synth|theta_k2|theta_syn_k2|phi_fwd_k2|phi_inv_k2" -c 16 \
   -o $O/${T}_full python bench.py --steps 1 --warmup 3 --no-cpu > $O/${T}_ncu_full.log 2>&1
-tail -3 $O/${T}_pytest.log
+# the two-set DMMA analysis launch of the wavelet synthesis (not among the first 16)
+ncu --set full --import-source on --clock-control none -k regex:"leg_ana_dmma" -c 2 \
+  -o $O/${T}_dmma python bench.py --steps 1 --warmup 3 --no-cpu > $O/${T}_ncu_dmma.log 2>&1
+tail -3 $O/${T}_pytest.log; tail -1 $O/${T}_smoke.log
