@@ -932,6 +932,51 @@ __global__ void __launch_bounds__(T, S2W_K2_PHIF_MINB) phi_fwd_k2_kernel(PhiFwdA
     __syncthreads();
   }
   pfa4095<false>(buf, tid, T);
+  // Bin mi sits at slot 2174 mi mod N (pfa_pos is additive: the slot advances
+  // by pfa_pos(T) per iteration).  Plain [set][bin][ring] output (no shard
+  // offset tables): the row pointer advances by T rows per iteration and the
+  // loop is unrolled so the shared-memory gathers of four bins are in flight
+  // before the first store.
+  const bool plain = !a.ofs && !a.peer_q;
+  constexpr int dpos = (int)(((unsigned)T * (unsigned)PFA_STEP) % (unsigned)PFA_N);
+  if (!a.real && plain) {
+    double2* o = a.out + ((size_t)set * a.n_bins + tid) * a.n_rings + ta;
+    const size_t step = (size_t)T * a.n_rings;
+    const double sc = a.scale;
+    int pos = pfa_pos(tid);
+#pragma unroll 4
+    for (int mi = tid; mi < a.n_bins; mi += T) {
+      *o = cscale(buf[pos], sc);
+      o += step;
+      pos = pfa_next(pos, dpos);
+    }
+    return;
+  }
+  if (a.real && plain) {
+    double2* o = a.out + ((size_t)set * a.n_bins + tid) * a.n_rings + ta;
+    const size_t step = (size_t)T * a.n_rings;
+    const double h = 0.5 * a.scale;
+    // the ring pair as one 32-byte sector (the row step is a multiple of 32 bytes)
+    const bool pair = vb && aligned32(o);
+    int pos = pfa_pos(tid);
+    int posr = pfa_pos(N - tid);  // slot of the mirror bin N - mi (bin 0: pfa_pos(N) = 0, itself)
+#pragma unroll 4
+    for (int mi = tid; mi < a.n_bins; mi += T) {
+      const double2 z = buf[pos];
+      const double2 zr = cconj(buf[posr]);
+      const double2 r0 = cscale(cadd(z, zr), h), r1 = cscale(cmul_mi(csub(z, zr)), h);
+      if (pair) st_global_32(o, r0, r1);
+      else {
+        o[0] = r0;
+        if (vb) o[1] = r1;
+      }
+      o += step;
+      pos = pfa_next(pos, dpos);
+      posr -= dpos;  // bin N - (mi + T)
+      if (posr < 0) posr += PFA_N;
+    }
+    return;
+  }
   for (int mi = tid; mi < a.n_bins; mi += T) {
     const double2 z = buf[pfa_pos(mi)];
     if (!a.real) {
@@ -1014,8 +1059,12 @@ __global__ void __launch_bounds__(T, S2W_K2_PHI_MINB + 1) phi_inv_k2_kernel(PhiI
   const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
   const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
   const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+  constexpr int dpos = (int)(((unsigned)T * (unsigned)PFA_STEP) % (unsigned)PFA_N);
+  int pos = pfa_pos(tid);  // slot of sample q: advances by pfa_pos(T) per iteration
+#pragma unroll 4
   for (int q = tid; q < N; q += T) {
-    const double2 v = buf[pfa_pos(q)];
+    const double2 v = buf[pos];
+    pos = pfa_next(pos, dpos);
     if (a.real) {
       a.out[ob + q] = hard_thresh(pa ? pva.x : v.x, a.thresh);
       if (vb) a.out[ob + N + q] = hard_thresh(pb ? pvb.x : v.y, a.thresh);
@@ -1081,7 +1130,15 @@ __global__ void __launch_bounds__(T, S2W_K2_TSYN_MINB) theta_syn_k2_kernel(Theta
   __syncthreads();
   // 4. inverse DFT_N by the prime-factor engine; rings t and N-1-t
   pfa4095<true>(buf, tid, T);
-  for (int t = tid; t < k; t += T) theta_syn_store(R, a, t, buf[pfa_pos(t)], buf[pfa_pos(N - 1 - t)]);
+  constexpr int dpos = (int)(((unsigned)T * (unsigned)PFA_STEP) % (unsigned)PFA_N);
+  int pos = pfa_pos(tid), posr = pfa_pos(N - 1 - tid);  // slots of rings t and N-1-t
+#pragma unroll 4
+  for (int t = tid; t < k; t += T) {
+    theta_syn_store(R, a, t, buf[pos], buf[posr]);
+    pos = pfa_next(pos, dpos);
+    posr -= dpos;
+    if (posr < 0) posr += PFA_N;
+  }
 }
 
 template <int T>
@@ -1154,6 +1211,7 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
   const RaderTabs R = rader_tabs(a.T);
   double2 x0, X0;
   rader8191<T, false>(buf, R, part, x0, X0);
+#pragma unroll 4
   for (int mi = tid; mi < a.n_bins; mi += T) {
     const double2 z = rader_bin<false>(buf, R, x0, X0, mi);
     if (!a.real) {
@@ -1230,6 +1288,7 @@ __global__ void __launch_bounds__(T, 1) phi_inv_k4_kernel(PhiInvArgs a) {
   const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
   const double2 pvb = pb ? __ldg(&Gb[0]) : make_double2(0.0, 0.0);
   const size_t ob = ((size_t)set * a.n_rings + ta) * N;
+#pragma unroll 4
   for (int q = tid; q < N; q += T) {
     const double2 v = rader_bin<true>(buf, R, x0, X0, q);
     if (a.real) {
@@ -1300,6 +1359,7 @@ __global__ void __launch_bounds__(T, 1) theta_syn_k4_kernel(ThetaSynArgs a) {
   const RaderTabs R = rader_tabs(F);
   double2 x0, X0;
   rader8191<T, true>(buf, R, part, x0, X0);
+#pragma unroll 4
   for (int t = tid; t < k; t += T)
     theta_syn_store(Rw, a, t, rader_bin<true>(buf, R, x0, X0, t), rader_bin<true>(buf, R, x0, X0, N - 1 - t));
 }

@@ -189,6 +189,7 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   // 8. direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
   fft_fwd<12, T, 0>(buf, tw, tid);
   const ThetaPair P = theta_pair(a, row, true);
+#pragma unroll 4
   for (int t = tid; t < k; t += T) {
     const double2 wt = cconj(buf[swz(fft_brev<12>(t))]);
     const double2 wr = cconj(buf[swz(fft_brev<12>(K2_M - 1 - t))]);
