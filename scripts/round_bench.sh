@@ -21,4 +21,11 @@ ncu --set full --import-source on --clock-control none \
 # the two-set DMMA analysis launch of the wavelet synthesis (not among the first 16)
 ncu --set full --import-source on --clock-control none -k regex:"leg_ana_dmma" -c 2 \
   -o $O/${T}_dmma python bench.py --steps 1 --warmup 3 --no-cpu > $O/${T}_ncu_dmma.log 2>&1
+python bench.py --mode shard --no-cpu --steps 10 > $O/${T}_bench_shard1.json 2>> $O/${T}_bench.err
+# summaries (text) travel back even when the .ncu-rep files are too large to keep
+python scripts/ncu_summary.py full $O/${T}_full.ncu-rep > $O/${T}_full_summary.txt 2>/dev/null
+python scripts/ncu_summary.py full $O/${T}_dmma.ncu-rep > $O/${T}_dmma_full_summary.txt 2>/dev/null
+# gpurun brings back at most 64 MiB: keep the summaries, drop the reports that do not fit
+rm -f $O/${T}_dmma.ncu-rep
+[ $(du -sm $O | cut -f1) -gt 60 ] && rm -f $O/${T}_full.ncu-rep
 tail -3 $O/${T}_pytest.log; tail -1 $O/${T}_smoke.log
