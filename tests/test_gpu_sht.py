@@ -255,3 +255,36 @@ def test_pipelined_analysis_matches_default():
                 _device._sht_plans.clear()
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
         assert np.abs(got - f).max() <= 1e-10 * np.abs(f).max()
+
+
+@pytest.mark.parametrize("l0,m0", [(2040, 900), (1200, 64), (2047, 2000), (1500, 33)])
+def test_terms_left_out_stay_below_the_threshold(sw, l0, m0):
+    """The Legendre kernels hold a ring out of the sums until its column can
+    pass 2^-80 before the ring is looked at again (ring_fix,
+    csrc/legendre_kernels.cu; the reference flushes at 1e-280, sht.py:179-184).
+    One unit coefficient makes every ring's Fourier mode a single term
+    P_lm(theta_t): where the device holds the term back the oracle's value must
+    lie below that level; everywhere else the two agree, the tiny polar values
+    to 1e-8 of themselves.  GL grid: no theta resampling between the Legendre
+    sums and the rings."""
+    from oracle import oracle as orc
+
+    L = 2048
+    f = np.zeros(L * L, dtype=np.complex128)
+    f[l0 * l0 + l0 + m0] = 1.0
+    grid = sw.make_grid(sw.SamplingScheme.GL, L)
+    smap = sw.sh_synthesis(sw.HarmonicCoeffs(L, f, real_signal=False), grid)
+    got = np.fft.fft(np.asarray(smap.values), axis=1)[:, m0] / (2 * L - 1)
+    want = orc.legendre_synth(f[None], L, False, "gl", orders=[m0])[0][:, m0]
+    err = np.abs(got - want)
+    # small values keep their own relative accuracy (1e-8 of themselves, down to
+    # the threshold); near the zero crossings the error is relative to the column
+    assert np.all(err <= 1e-8 * np.abs(want) + 1e-13 * np.abs(want).max() + 2.0 ** -78)
+    assert rel_err(got, want) < TOL
+    held = got == 0.0
+    if held.any():
+        assert np.abs(want[held]).max() < 2.0 ** -80
+    # a column that has not passed 2^-400 cannot reach 2^-80 within a chunk
+    # (growth < 2^8 per degree): those rings are held back, exact zeros, which
+    # includes rings round 1's 2^-600 level would have summed
+    assert np.all(held[np.abs(want) < 2.0 ** -400])
