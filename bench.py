@@ -623,7 +623,7 @@ def run_reference(args, cfgname):
                                   cfg["batch"] * cfg["L"] * (2 * cfg["L"] - 1)
                                   * (8 if cfg["real"] else 16)),
         "cpu_baseline": {"value": v, "unit": "round-trips/s", "cores": s0["cores"],
-                         "kind": s0["kind"], "sample": s0["sample"]},
+                         "kind": s0["kind"], "coverage": s0["coverage"], "sample": s0["sample"]},
         "e2e": {"value": v, "unit": "round-trips/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
