@@ -262,8 +262,20 @@ static void fft_ld(std::vector<cld>& a) {
 
 static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
 
-// spectrum (natural order) / M, stored at bit-reversed positions.  Split mode
-// (M > 2^FFT_MAX_LOGM_SMEM): [even half | odd half], each bit-reversed over M/2.
+// spectrum (natural order) / M, stored at bit-reversed positions and then
+// transposed for the core pass.  Split mode (M > 2^FFT_MAX_LOGM_SMEM):
+// [even half | odd half], each bit-reversed over M/2.
+// The table is read only by the engine's core pass (fft.cuh conv_core*),
+// whose thread b multiplies the R = 2^CB consecutive elements b R + i: entry
+// (b, i) is stored at i (E / R) + b (E the engine size), so the 32 lanes of a
+// warp read 32 consecutive entries instead of 32 separate lines.
+static void core_transpose(double2* t, int log_e) {
+  const int cb = log_e - 4 * ((log_e - 1) / 4);
+  const size_t R = (size_t)1 << cb, NB = ((size_t)1 << log_e) / R;
+  std::vector<double2> tmp(t, t + R * NB);
+  for (size_t b = 0; b < NB; ++b)
+    for (size_t i = 0; i < R; ++i) t[i * NB + b] = tmp[b * R + i];
+}
 static std::vector<double2> spectrum_brev(std::vector<cld> a) {
   const size_t M = a.size();
   const int bits = ilog2_ceil((long long)M);
@@ -271,6 +283,7 @@ static std::vector<double2> spectrum_brev(std::vector<cld> a) {
   std::vector<double2> out(M);
   if (bits <= FFT_MAX_LOGM_SMEM) {
     for (size_t p = 0; p < M; ++p) out[p] = d2(a[bitrev((unsigned)p, bits)] / (ld)M);
+    core_transpose(out.data(), bits);
   } else {
     const size_t F = M / 2;
     for (size_t p = 0; p < F; ++p) {
@@ -278,6 +291,8 @@ static std::vector<double2> spectrum_brev(std::vector<cld> a) {
       out[p] = d2(a[2 * k] / (ld)M);
       out[F + p] = d2(a[2 * k + 1] / (ld)M);
     }
+    core_transpose(out.data(), bits - 1);
+    core_transpose(out.data() + F, bits - 1);
   }
   return out;
 }

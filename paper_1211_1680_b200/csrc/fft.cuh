@@ -173,7 +173,9 @@ S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, i
 }
 
 // Core pass: last forward pass (radix 2^CB, span 1), product with the
-// bit-reversed spectrum table, first inverse pass.
+// bit-reversed spectrum table, first inverse pass.  The table is stored
+// transposed, entry (b, i) at i NB + b (capi.cu core_transpose): a warp's
+// loads are contiguous.
 template <int LOGM, int GS>
 S2W_DEV void conv_core(double2* __restrict__ buf, const double2* __restrict__ tab, int gtid) {
   constexpr int CB = LOGM - 4 * fft_k16(LOGM);
@@ -189,7 +191,7 @@ S2W_DEV void conv_core(double2* __restrict__ buf, const double2* __restrict__ ta
     for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];
     dif<CB>(v);
 #pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], __ldg(&tab[b * R + i]));
+    for (int i = 0; i < R; ++i) v[i] = cmul(v[i], __ldg(&tab[i * NB + b]));
     adj<CB>(v);
 #pragma unroll
     for (int i = 0; i < R; ++i) buf[sb ^ swz(i)] = v[i];
@@ -210,7 +212,7 @@ S2W_DEV void conv_core_real(double2* __restrict__ buf, const double* __restrict_
     const int sb = swz(b * R);
     double t[R];
 #pragma unroll
-    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[b * R + i]);
+    for (int i = 0; i < R; ++i) t[i] = __ldg(&tab[i * NB + b]);
     double2 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = buf[sb ^ swz(i)];

@@ -872,6 +872,15 @@ constexpr int K2_T = S2W_K2_T;
 #define S2W_K2_TT 256
 #endif
 constexpr int K2_TT = S2W_K2_TT;  // theta_k2 threads
+#ifndef S2W_K2_PFT
+#define S2W_K2_PFT S2W_K2_T
+#endif
+#ifndef S2W_K2_PIT
+#define S2W_K2_PIT S2W_K2_T
+#endif
+// ring-DFT CTA sizes: the prime-factor passes have 315 / 585 / 819 / 455 lines,
+// so 320 threads take 1 + 2 + 3 + 2 rounds where 256 take 2 + 3 + 4 + 2
+constexpr int K2_PFT = S2W_K2_PFT, K2_PIT = S2W_K2_PIT;
 #ifndef S2W_K2_PHI_MINB
 #define S2W_K2_PHI_MINB 2
 #endif
@@ -1615,7 +1624,7 @@ cudaError_t launch_phi_fwd(PhiFwdArgs a, cudaStream_t st) {
   if (use_k4(a.T) && k2_ok(a.in, a.real, a.n_rings))
     return k2_launch(phi_fwd_k4_kernel<K4_T>, a, n_rows, k4_smem(0, false), st, K4_T);
   if (use_pfa(a.T.N) && k2_ok(a.in, a.real, a.n_rings))
-    return k2_launch(phi_fwd_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
+    return k2_launch(phi_fwd_k2_kernel<K2_PFT>, a, n_rows, k2_smem(0, false), st, K2_PFT);
   if (use_pfa(a.T.N)) return pfa_launch(phi_fwd_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_fwd_kernel, phi_fwd_split_kernel, a, n_rows, st)
 }
@@ -1626,7 +1635,7 @@ cudaError_t launch_phi_inv(PhiInvArgs a, cudaStream_t st) {
   if (use_k4(a.T) && k2_ok(a.in, false, a.n_rings) && a.n_bins <= (a.real ? K4_K : K4_N))
     return k2_launch(phi_inv_k4_kernel<K4_T>, a, n_rows, k4_smem(0, false), st, K4_T);
   if (use_pfa(a.T.N) && k2_ok(a.in, false, a.n_rings) && a.n_bins <= (a.real ? K2_K : K2_N))
-    return k2_launch(phi_inv_k2_kernel<K2_T>, a, n_rows, k2_smem(0, false), st);
+    return k2_launch(phi_inv_k2_kernel<K2_PIT>, a, n_rows, k2_smem(0, false), st, K2_PIT);
   if (use_pfa(a.T.N)) return pfa_launch(phi_inv_pfa_kernel, a, n_rows, st);
   S2W_FFT_DISPATCH(phi_inv_kernel, phi_inv_split_kernel, a, n_rows, st)
 }
