@@ -131,6 +131,32 @@ S2W_DEV void powers16(double2* w, double2 u) {
   for (int k = 1; k < 8; ++k) w[8 + k] = cmul(w[8], w[k]);
 }
 
+// The register part of one radix-16 pass with pass twiddle u = W_{16 s}^j.
+// Forward: v[k] = element j + k s in, register i = output brev4(i) out (the
+// in-place DIF layout).  INV: the adjoint, that layout in, natural out.
+template <bool INV>
+S2W_DEV void bfly16(double2* v, double2 u) {
+  // twiddle powers u^1..u^7 and u^8; u^(8+k) = u^8 u^k formed at use (the
+  // same products as powers16, with half of them live at a time)
+  double2 w[8];
+  w[1] = u;
+  w[2] = cmul(u, u);
+  w[3] = cmul(w[2], u);
+  w[4] = cmul(w[2], w[2]);
+  w[5] = cmul(w[4], u);
+  w[6] = cmul(w[4], w[2]);
+  w[7] = cmul(w[4], w[3]);
+  const double2 w8 = cmul(w[4], w[4]);
+  if constexpr (!INV) dif<4>(v);
+#pragma unroll
+  for (int kk = 1; kk < 16; ++kk) {
+    const double2 wk = kk < 8 ? w[kk] : (kk == 8 ? w8 : cmul(w8, w[kk - 8]));
+    const int i = brev4(kk);
+    v[i] = INV ? cmulc(v[i], wk) : cmul(v[i], wk);
+  }
+  if constexpr (INV) adj<4>(v);
+}
+
 // One radix-16 pass at span 2^LS (forward DIF, or its adjoint when INV).
 // TWS: stride into the twiddle table (2 when a half-size transform borrows
 // the table of the engine size: W_{16s}^j = W_{32s}^{2j}).
@@ -147,26 +173,7 @@ S2W_DEV void pass16(double2* __restrict__ buf, const double2* __restrict__ tw, i
     double2 v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = buf[sb ^ swz(k << LS)];
-    // twiddle powers u^1..u^7 and u^8; u^(8+k) = u^8 u^k formed at use (the
-    // same products as powers16, with half of them live at a time)
-    double2 w[8];
-    const double2 u = tw[j * TWS];
-    w[1] = u;
-    w[2] = cmul(u, u);
-    w[3] = cmul(w[2], u);
-    w[4] = cmul(w[2], w[2]);
-    w[5] = cmul(w[4], u);
-    w[6] = cmul(w[4], w[2]);
-    w[7] = cmul(w[4], w[3]);
-    const double2 w8 = cmul(w[4], w[4]);
-    if constexpr (!INV) dif<4>(v);
-#pragma unroll
-    for (int kk = 1; kk < 16; ++kk) {
-      const double2 wk = kk < 8 ? w[kk] : (kk == 8 ? w8 : cmul(w8, w[kk - 8]));
-      const int i = brev4(kk);
-      v[i] = INV ? cmulc(v[i], wk) : cmul(v[i], wk);
-    }
-    if constexpr (INV) adj<4>(v);
+    bfly16<INV>(v, tw[j * TWS]);
 #pragma unroll
     for (int k = 0; k < 16; ++k) buf[sb ^ swz(k << LS)] = v[k];
   }

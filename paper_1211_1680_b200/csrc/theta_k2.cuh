@@ -79,6 +79,19 @@ S2W_DEV void k2_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* ds
   if (go) bulk_g2s(dst + K2_K, go, col, mb);
 }
 
+// A 4096-point cyclic convolution without its outer radix-16 passes: the
+// forward pass at span 16, the core pass with the real spectrum table and the
+// inverse pass at span 16.  Ends synced.
+template <int T>
+S2W_DEV void conv12_inner(double2* buf, const double2* tw, const double* __restrict__ tab, int tid) {
+  pass16<12, T, 4, false>(buf, tw + fft_tw_off(12, 1), tid);
+  __syncthreads();
+  conv_core_real<12, T>(buf, tab, tid);
+  __syncthreads();
+  pass16<12, T, 4, true>(buf, tw + fft_tw_off(12, 1), tid);
+  __syncthreads();
+}
+
 // One theta column pair (row `row` of a) on the CTA's T threads.  smem:
 // k2_theta_smem_bytes() of 16-byte aligned shared memory.  pf > 0: also
 // prefetch row + pf into L2.  Precondition: every thread is done with smem
@@ -149,31 +162,43 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   for (int s = 1024 + tid; s <= 3072; s += T) buf[swz(s)] = make_double2(0.0, 0.0);
   __syncthreads();
   // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
-  //      a); in between, even outputs -> side, odd coefficients -> buf
-#pragma unroll 1
-  for (int cls = 0; cls < 2; ++cls) {
-    fft_conv_real<12, T>(buf, tw, F.w2s, tid);
-    if (cls) break;
-    double2 ev[V], od[V];
+  //      a).  Thread tid owns the elements tid + 256 k of both outer radix-16
+  //      passes, so the last inverse pass of the even class, the class swap
+  //      (even outputs -> side, odd coefficients -> buf) and the first forward
+  //      pass of the odd class run in registers with no barrier in between.
+  static_assert(T == 256, "one outer radix-16 butterfly per thread");
+  const int sb = swz(tid);
+  pass16<12, T, 8, false>(buf, tw, tid);
+  __syncthreads();
+  conv12_inner<T>(buf, tw, F.w2s, tid);
+  {
+    double2 v[16];
 #pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = tid + u * T;
-      const int aa = i < 1024 ? i : i - 2048;
-      ev[u] = buf[swz(aa & (K2_M - 1))];
-      od[u] = side[aa & (K2_K - 1)];
-    }
-    __syncthreads();
+    for (int kk = 0; kk < 16; ++kk) v[kk] = buf[sb ^ swz(kk << 8)];
+    const double2 u = tw[tid];
+    bfly16<true>(v, u);  // v[kk] = H'(2a), a = tid + 256 kk (mod 4096)
 #pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = tid + u * T;
-      const int aa = i < 1024 ? i : i - 2048;
-      buf[swz(aa & (K2_M - 1))] = od[u];
-      side[aa & (K2_K - 1)] = ev[u];
-      buf[swz(1024 + i)] = make_double2(0.0, 0.0);
+    for (int kk = 0; kk < 16; ++kk) {
+      if (kk >= 4 && kk < 12) {
+        v[kk] = make_double2(0.0, 0.0);  // |a| >= 1024: not needed / zero padding
+      } else {
+        const int sl = (tid + 256 * kk) & (K2_K - 1);
+        const double2 od = side[sl];
+        side[sl] = v[kk];
+        v[kk] = od;
+      }
     }
-    __syncthreads();
+    bfly16<false>(v, u);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk << 8)] = v[kk];
   }
-  // 7. evaluation on the analysis rings: X'_n = conj(H'(q)) e^{-i pi q/N2}, n = q mod N2
+  __syncthreads();
+  conv12_inner<T>(buf, tw, F.w2s, tid);
+  pass16<12, T, 8, true>(buf, tw, tid);
+  __syncthreads();
+  // 7. evaluation on the analysis rings: X'_n = conj(H'(q)) e^{-i pi q/N2}, n = q mod N2.
+  //    x[u] is element tid + 256 u: the input of this thread's first radix-16
+  //    butterfly of the length-N2 FFT (8), which therefore runs in registers.
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int n = tid + u * T;
@@ -183,11 +208,15 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
     x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
   }
   __syncthreads();
+  bfly16<false>(x, tw[tid]);
 #pragma unroll
-  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
+  for (int u = 0; u < U; ++u) buf[sb ^ swz(u << 8)] = x[u];
   __syncthreads();
-  // 8. direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
-  fft_fwd<12, T, 0>(buf, tw, tid);
+  // 8. the rest of the direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
+  pass16<12, T, 4, false>(buf, tw + fft_tw_off(12, 1), tid);
+  __syncthreads();
+  fwd_core<12, T>(buf, tid);
+  __syncthreads();
   const ThetaPair P = theta_pair(a, row, true);
 #pragma unroll 4
   for (int t = tid; t < k; t += T) {
