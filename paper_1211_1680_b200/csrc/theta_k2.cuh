@@ -144,32 +144,42 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   // 2. DFT_N
   pfa4095<false>(buf, tid, T);
   // 3. Fourier coefficients a_q = X_bin e^{-i pi q/N} / N by parity of q:
-  //    even q = 2b -> buf slot b (mod 4096), odd q = 2b+1 -> side slot b (mod 2048)
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int bin = tid + u * T;
-    x[u] = bin < N ? cmul(buf[pfa_pos(bin)], __ldg(&F.phA[bin])) : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int bin = tid + u * T;
-    if (bin >= N) continue;
-    const int q = bin < k ? bin : bin - N;
-    if (q & 1) side[((q - 1) >> 1) & (K2_K - 1)] = x[u];
-    else buf[swz((q >> 1) & (K2_M - 1))] = x[u];
-  }
-  for (int s = 1024 + tid; s <= 3072; s += T) buf[swz(s)] = make_double2(0.0, 0.0);
-  __syncthreads();
-  // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
-  //      a).  Thread tid owns the elements tid + 256 k of both outer radix-16
-  //      passes, so the last inverse pass of the even class, the class swap
-  //      (even outputs -> side, odd coefficients -> buf) and the first forward
-  //      pass of the odd class run in registers with no barrier in between.
+  //    even q = 2a -> element a (mod 4096) of the even-class row in buf, odd
+  //    q = 2a+1 -> side slot a (mod 2048).  Thread tid gathers the elements
+  //    tid + 256 kk of both classes (|a| < 1024: kk in 0..3 and 12..15; the
+  //    rest is the zero padding), which are the inputs of its first radix-16
+  //    butterfly of the even-class convolution (4): that pass runs in
+  //    registers, with no zero fill and no extra trip through shared memory.
+  //    Thread tid owns the elements tid + 256 k of every outer radix-16 pass.
   static_assert(T == 256, "one outer radix-16 butterfly per thread");
   const int sb = swz(tid);
-  pass16<12, T, 8, false>(buf, tw, tid);
+  {
+    double2 v[16], vo[8];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      if (kk >= 4 && kk < 12) {
+        v[kk] = make_double2(0.0, 0.0);
+        continue;
+      }
+      const int aa = tid + 256 * kk - (kk < 4 ? 0 : K2_M);  // [-1024, 1024)
+      const int be = 2 * aa + (aa < 0 ? N : 0);             // bin of q = 2 aa
+      const int bo = be + 1;                                // bin of q = 2 aa + 1
+      v[kk] = aa > -1024 ? cmul(buf[pfa_pos(be)], __ldg(&F.phA[be])) : make_double2(0.0, 0.0);
+      vo[kk & 7] = cmul(buf[pfa_pos(bo)], __ldg(&F.phA[bo]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+      if (kk < 4 || kk >= 12) side[(tid + 256 * kk) & (K2_K - 1)] = vo[kk & 7];
+    bfly16<false>(v, tw[tid]);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk << 8)] = v[kk];
+  }
   __syncthreads();
+  // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
+  //      a): the last inverse pass of the even class, the class swap (even
+  //      outputs -> side, odd coefficients -> buf) and the first forward pass
+  //      of the odd class run in registers with no barrier in between.
   conv12_inner<T>(buf, tw, F.w2s, tid);
   {
     double2 v[16];
