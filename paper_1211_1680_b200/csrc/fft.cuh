@@ -243,12 +243,12 @@ S2W_DEV void fwd_passes(double2* buf, const double2* tw, int gtid) {
     fwd_passes<LOGM, GS, P + 1, TWSH>(buf, tw, gtid);
   }
 }
-template <int LOGM, int GS, int P>
+template <int LOGM, int GS, int P, int PMIN = 0>
 S2W_DEV void inv_passes(double2* buf, const double2* tw, int gtid) {
-  if constexpr (P >= 0) {
+  if constexpr (P >= PMIN) {
     pass16<LOGM, GS, LOGM - 4 * (P + 1), true>(buf, tw + fft_tw_off(LOGM, P), gtid);
     __syncthreads();
-    inv_passes<LOGM, GS, P - 1>(buf, tw, gtid);
+    inv_passes<LOGM, GS, P - 1, PMIN>(buf, tw, gtid);
   }
 }
 
@@ -304,6 +304,35 @@ S2W_DEV void fft_conv_real(double2* buf, const double2* tw, const double* __rest
   conv_core_real<LOGM, GS>(buf, tab, gtid);
   __syncthreads();
   inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
+}
+
+// fft_conv_real without its outer radix-16 passes (the first forward and the
+// last inverse pass, at span 2^(LOGM-4)): for callers whose GS = 2^(LOGM-4)
+// threads run those two in registers (thread j owns the elements j + GS k of
+// both) around their own data movement.  Row synced on entry; ends synced.
+template <int LOGM, int GS>
+S2W_DEV void fft_conv_real_inner(double2* buf, const double2* tw, const double* __restrict__ tab,
+                                 int gtid) {
+  fwd_passes<LOGM, GS, 1>(buf, tw, gtid);
+  conv_core_real<LOGM, GS>(buf, tab, gtid);
+  __syncthreads();
+  inv_passes<LOGM, GS, fft_k16(LOGM) - 1, 1>(buf, tw, gtid);
+}
+
+// Forward DFT (as fft_fwd) whose first radix-16 pass input the caller holds in
+// registers: v[k] = element gtid + GS k, GS = 2^(LOGN-4).  Every thread must
+// be done reading the row (a barrier) before the call.  Ends synced.
+template <int LOGN, int GS>
+S2W_DEV void fft_fwd_from_regs(double2* buf, const double2* tw, double2* v, int gtid) {
+  static_assert(GS == (1 << (LOGN - 4)), "one outer butterfly per thread");
+  bfly16<false>(v, tw[gtid]);
+  const int sb = swz(gtid);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) buf[sb ^ swz(k << (LOGN - 4))] = v[k];
+  __syncthreads();
+  fwd_passes<LOGN, GS, 1, 0>(buf, tw, gtid);
+  fwd_core<LOGN, GS>(buf, gtid);
+  __syncthreads();
 }
 
 // Copy the pass twiddles into shared memory (all threads of the CTA).

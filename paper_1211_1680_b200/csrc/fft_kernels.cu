@@ -1115,11 +1115,9 @@ __global__ void __launch_bounds__(T, S2W_K2_TSYN_MINB) theta_syn_k2_kernel(Theta
     x[u] = lo ? cadd(e, o) : csub(e, o);
   }
   __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
-  __syncthreads();
-  // 2. DFT_4096 (direct)
-  fft_fwd<12, T, 0>(buf, tw, tid);
+  // 2. DFT_4096 (direct).  x[u] is element tid + 256 u, the input of this
+  //    thread's first radix-16 butterfly: that pass runs in registers.
+  fft_fwd_from_regs<12, T>(buf, tw, x, tid);
   // 3. DFT_N input (bit-reversed source slot, n >= k reads bin n + 1)
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -1345,10 +1343,8 @@ __global__ void __launch_bounds__(T, 1) theta_syn_k4_kernel(ThetaSynArgs a) {
     x[u] = lo ? cadd(e, o) : csub(e, o);
   }
   __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
-  __syncthreads();
-  fft_fwd<13, T, 0>(buf, tw, tid);
+  // x[u] is element tid + 512 u: the first radix-16 pass runs in registers
+  fft_fwd_from_regs<13, T>(buf, tw, x, tid);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int n = tid + u * T;
@@ -1381,7 +1377,7 @@ __global__ void __launch_bounds__(T, 1) theta_k4_kernel(ThetaArgs a) {
   double2* tw = side + K4_K;         // [546]
   double2* part = tw + K4_NTW;       // [T/32]
   uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
-  constexpr int N = K4_N, k = K4_K, U = K4_M / T, V = K4_K / T;
+  constexpr int N = K4_N, k = K4_K, U = K4_M / T;
   const FftTablesDev& F = a.T;
   const int tid = threadIdx.x;
   bool has_e, has_o;
@@ -1415,63 +1411,11 @@ __global__ void __launch_bounds__(T, 1) theta_k4_kernel(ThetaArgs a) {
   const RaderTabs R = rader_tabs(F);
   double2 x0, X0;
   rader8191<T, false>(buf, R, part, x0, X0);
-  // 3. coefficients by parity of q (see theta_k2)
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int bin = tid + u * T;
-    x[u] = bin < N ? cmul(rader_bin<false>(buf, R, x0, X0, bin), __ldg(&F.phA[bin]))
-                   : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int bin = tid + u * T;
-    if (bin >= N) continue;
-    const int q = bin < k ? bin : bin - N;
-    if (q & 1) side[((q - 1) >> 1) & (K4_K - 1)] = x[u];
-    else buf[swz((q >> 1) & (K4_M - 1))] = x[u];
-  }
-  for (int s2 = 2048 + tid; s2 <= 6144; s2 += T) buf[swz(s2)] = make_double2(0.0, 0.0);
-  __syncthreads();
-  // 4-6. even class, swap, odd class
-#pragma unroll 1
-  for (int cls = 0; cls < 2; ++cls) {
-    fft_conv_real<13, T>(buf, tw, F.w4s, tid);
-    if (cls) break;
-    double2 ev[V], od[V];
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = tid + u * T;
-      const int aa = i < 2048 ? i : i - 4096;
-      ev[u] = buf[swz(aa & (K4_M - 1))];
-      od[u] = side[aa & (K4_K - 1)];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = tid + u * T;
-      const int aa = i < 2048 ? i : i - 4096;
-      buf[swz(aa & (K4_M - 1))] = od[u];
-      side[aa & (K4_K - 1)] = ev[u];
-      buf[swz(2048 + i)] = make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-  }
-  // 7. evaluation input X'_n = conj(H'(q)) e^{-i pi q/N2}
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    const int q = n < k ? n : n - K4_M;
-    double2 h = make_double2(0.0, 0.0);
-    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (K4_M - 1))] : side[(q >> 1) & (K4_K - 1)];
-    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) buf[swz(tid + u * T)] = x[u];
-  __syncthreads();
-  // 8. direct FFT of length N2 = 8192; rings j and N2-1-j, split by parity
-  fft_fwd<13, T, 0>(buf, tw, tid);
+  // 3-8. coefficient split, parity-class convolutions, evaluation FFT
+  //      (N2 = 8192), as theta_k2; rings j and N2-1-j, split by parity
+  static_assert(U == 16, "theta_classes scratch");
+  theta_classes<13, T>(buf, side, tw, F, F.w4s, x,
+                       [&](int bin) { return rader_bin<false>(buf, R, x0, X0, bin); });
   const ThetaPair P = theta_pair(a, blockIdx.x, true);
   for (int t = tid; t < k; t += T) {
     const double2 wt = cconj(buf[swz(fft_brev<13>(t))]);

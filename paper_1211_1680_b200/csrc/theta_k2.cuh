@@ -79,17 +79,94 @@ S2W_DEV void k2_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* ds
   if (go) bulk_g2s(dst + K2_K, go, col, mb);
 }
 
-// A 4096-point cyclic convolution without its outer radix-16 passes: the
-// forward pass at span 16, the core pass with the real spectrum table and the
-// inverse pass at span 16.  Ends synced.
-template <int T>
-S2W_DEV void conv12_inner(double2* buf, const double2* tw, const double* __restrict__ tab, int tid) {
-  pass16<12, T, 4, false>(buf, tw + fft_tw_off(12, 1), tid);
+// Steps 3-8 of the theta column-pair transform on an engine of M = 2^LOGM
+// points (N = M - 1 MW samples on the circle, k = M/2 rings, T = M/16
+// threads): the Fourier coefficients a_q = X_bin e^{-i pi q/N} / N (X_bin =
+// bin_value(bin), the DFT_N of the extended pair) split by the parity of q,
+// the two parity-class |sin| convolutions, the evaluation input and the
+// length-M FFT on the analysis rings.  On return buf holds that FFT
+// (bit-reversed, swizzled) and every thread is synced.
+//
+// Thread tid owns the elements tid + T kk (kk = 0..15) of every outer
+// radix-16 pass (span T), so the data movement between the transforms runs in
+// the registers of those passes:
+//  * 3 -> 4: even q = 2a is element a (mod M) of the even-class row, odd
+//    q = 2a+1 goes to side slot a (mod k).  The thread gathers the elements
+//    tid + T kk of both classes (|a| < M/4: kk in 0..3 and 12..15, the rest
+//    is the zero padding) and feeds the even ones to its first butterfly: no
+//    zero fill, no extra trip through shared memory.
+//  * 4 -> 5 -> 6: the last inverse pass of the even class (H'(2a) at element
+//    a), the class swap (even outputs -> side, odd coefficients -> buf) and
+//    the first forward pass of the odd class, with no barrier in between.
+//  * 7 -> 8: X'_n = conj(H'(q)) e^{-i pi q/M}, n = q mod M, is gathered as
+//    element tid + T u: the input of the first butterfly of the FFT.
+// x: 16 registers of scratch.  Precondition: bin_value's source written and
+// synced.
+template <int LOGM, int T, class Bin>
+S2W_DEV void theta_classes(double2* buf, double2* side, const double2* tw, const FftTablesDev& F,
+                           const double* __restrict__ wtab, double2* x, Bin bin_value) {
+  constexpr int M = 1 << LOGM, k = M / 2, N = M - 1;
+  static_assert(T == M / 16, "one outer radix-16 butterfly per thread");
+  const int tid = threadIdx.x;
+  const int sb = swz(tid);
+  {
+    double2 vo[8];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      if (kk >= 4 && kk < 12) {
+        x[kk] = make_double2(0.0, 0.0);
+        continue;
+      }
+      const int aa = tid + T * kk - (kk < 4 ? 0 : M);  // [-M/4, M/4)
+      const int be = 2 * aa + (aa < 0 ? N : 0);        // bin of q = 2 aa
+      const int bo = be + 1;                           // bin of q = 2 aa + 1
+      x[kk] = aa > -(M / 4) ? cmul(bin_value(be), __ldg(&F.phA[be])) : make_double2(0.0, 0.0);
+      vo[kk & 7] = cmul(bin_value(bo), __ldg(&F.phA[bo]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+      if (kk < 4 || kk >= 12) side[(tid + T * kk) & (k - 1)] = vo[kk & 7];
+    bfly16<false>(x, tw[tid]);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk * T)] = x[kk];
+  }
   __syncthreads();
-  conv_core_real<12, T>(buf, tab, tid);
+  fft_conv_real_inner<LOGM, T>(buf, tw, wtab, tid);
+  {
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) x[kk] = buf[sb ^ swz(kk * T)];
+    const double2 u = tw[tid];
+    bfly16<true>(x, u);  // x[kk] = H'(2a), a = tid + T kk (mod M)
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      if (kk >= 4 && kk < 12) {
+        x[kk] = make_double2(0.0, 0.0);  // |a| >= M/4: not needed / zero padding
+      } else {
+        const int sl = (tid + T * kk) & (k - 1);
+        const double2 od = side[sl];
+        side[sl] = x[kk];
+        x[kk] = od;
+      }
+    }
+    bfly16<false>(x, u);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk * T)] = x[kk];
+  }
   __syncthreads();
-  pass16<12, T, 4, true>(buf, tw + fft_tw_off(12, 1), tid);
+  fft_conv_real_inner<LOGM, T>(buf, tw, wtab, tid);
+  pass16<LOGM, T, LOGM - 4, true>(buf, tw, tid);
   __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int n = tid + u * T;
+    const int q = n < k ? n : n - M;
+    double2 h = make_double2(0.0, 0.0);
+    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (M - 1))] : side[(q >> 1) & (k - 1)];
+    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
+  }
+  __syncthreads();
+  fft_fwd_from_regs<LOGM, T>(buf, tw, x, tid);
 }
 
 // One theta column pair (row `row` of a) on the CTA's T threads.  smem:
@@ -143,90 +220,10 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   __syncthreads();
   // 2. DFT_N
   pfa4095<false>(buf, tid, T);
-  // 3. Fourier coefficients a_q = X_bin e^{-i pi q/N} / N by parity of q:
-  //    even q = 2a -> element a (mod 4096) of the even-class row in buf, odd
-  //    q = 2a+1 -> side slot a (mod 2048).  Thread tid gathers the elements
-  //    tid + 256 kk of both classes (|a| < 1024: kk in 0..3 and 12..15; the
-  //    rest is the zero padding), which are the inputs of its first radix-16
-  //    butterfly of the even-class convolution (4): that pass runs in
-  //    registers, with no zero fill and no extra trip through shared memory.
-  //    Thread tid owns the elements tid + 256 k of every outer radix-16 pass.
-  static_assert(T == 256, "one outer radix-16 butterfly per thread");
-  const int sb = swz(tid);
-  {
-    double2 v[16], vo[8];
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      if (kk >= 4 && kk < 12) {
-        v[kk] = make_double2(0.0, 0.0);
-        continue;
-      }
-      const int aa = tid + 256 * kk - (kk < 4 ? 0 : K2_M);  // [-1024, 1024)
-      const int be = 2 * aa + (aa < 0 ? N : 0);             // bin of q = 2 aa
-      const int bo = be + 1;                                // bin of q = 2 aa + 1
-      v[kk] = aa > -1024 ? cmul(buf[pfa_pos(be)], __ldg(&F.phA[be])) : make_double2(0.0, 0.0);
-      vo[kk & 7] = cmul(buf[pfa_pos(bo)], __ldg(&F.phA[bo]));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk)
-      if (kk < 4 || kk >= 12) side[(tid + 256 * kk) & (K2_K - 1)] = vo[kk & 7];
-    bfly16<false>(v, tw[tid]);
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk << 8)] = v[kk];
-  }
-  __syncthreads();
-  // 4-6. even class (H'(2a) at slot a), then the odd class (H'(2a+1) at slot
-  //      a): the last inverse pass of the even class, the class swap (even
-  //      outputs -> side, odd coefficients -> buf) and the first forward pass
-  //      of the odd class run in registers with no barrier in between.
-  conv12_inner<T>(buf, tw, F.w2s, tid);
-  {
-    double2 v[16];
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) v[kk] = buf[sb ^ swz(kk << 8)];
-    const double2 u = tw[tid];
-    bfly16<true>(v, u);  // v[kk] = H'(2a), a = tid + 256 kk (mod 4096)
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      if (kk >= 4 && kk < 12) {
-        v[kk] = make_double2(0.0, 0.0);  // |a| >= 1024: not needed / zero padding
-      } else {
-        const int sl = (tid + 256 * kk) & (K2_K - 1);
-        const double2 od = side[sl];
-        side[sl] = v[kk];
-        v[kk] = od;
-      }
-    }
-    bfly16<false>(v, u);
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk << 8)] = v[kk];
-  }
-  __syncthreads();
-  conv12_inner<T>(buf, tw, F.w2s, tid);
-  pass16<12, T, 8, true>(buf, tw, tid);
-  __syncthreads();
-  // 7. evaluation on the analysis rings: X'_n = conj(H'(q)) e^{-i pi q/N2}, n = q mod N2.
-  //    x[u] is element tid + 256 u: the input of this thread's first radix-16
-  //    butterfly of the length-N2 FFT (8), which therefore runs in registers.
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    const int q = n < k ? n : n - K2_M;
-    double2 h = make_double2(0.0, 0.0);
-    if (q > -k) h = (q & 1) ? buf[swz(((q - 1) >> 1) & (K2_M - 1))] : side[(q >> 1) & (K2_K - 1)];
-    x[u] = cmul(cconj(h), __ldg(&F.ph2d[n]));
-  }
-  __syncthreads();
-  bfly16<false>(x, tw[tid]);
-#pragma unroll
-  for (int u = 0; u < U; ++u) buf[sb ^ swz(u << 8)] = x[u];
-  __syncthreads();
-  // 8. the rest of the direct FFT of length N2 = 4096; rings j and N2-1-j, split by parity
-  pass16<12, T, 4, false>(buf, tw + fft_tw_off(12, 1), tid);
-  __syncthreads();
-  fwd_core<12, T>(buf, tid);
-  __syncthreads();
+  // 3-8. coefficient split, parity-class convolutions, evaluation FFT (N2 = 4096)
+  static_assert(U == 16, "theta_classes scratch");
+  theta_classes<12, T>(buf, side, tw, F, F.w2s, x, [&](int bin) { return buf[pfa_pos(bin)]; });
+  // rings j and N2-1-j, split by parity
   const ThetaPair P = theta_pair(a, row, true);
 #pragma unroll 4
   for (int t = tid; t < k; t += T) {
