@@ -799,7 +799,13 @@ static int build_grid(GridRes* g, int dev, int scheme, int k) {
     for (const double2& z : spectrum_brev(w2)) w2r.push_back(z.x);  // Im ~ 1e-19: exact zero
     CHECK(upload_new(&g->w2s, w2r));
     CHECK(upload_new(&g->phA, phA));
-    CHECK(upload_new(&g->phS, phS));
+    // theta_syn_k2 applies phS in the gather of the axis-9 prime-factor pass
+    // (pfa_pass_gather: line r, element j is sample (9 r + 455 j) mod N, read
+    // as entry j * 455 + r): stored in that order, a warp's loads are contiguous
+    std::vector<double2> phS9(N);
+    for (int r = 0; r < N / 9; ++r)
+      for (int j = 0; j < 9; ++j) phS9[(size_t)j * (N / 9) + r] = phS[(9 * r + j * (N / 9)) % N];
+    CHECK(upload_new(&g->phS, phS9));
   }
   if (N == 8191) {
     // k4 stage kernels: Rader's DFT_8191 over the prime-factor DFT_8190

@@ -1118,25 +1118,13 @@ __global__ void __launch_bounds__(T, S2W_K2_TSYN_MINB) theta_syn_k2_kernel(Theta
   // 2. DFT_4096 (direct).  x[u] is element tid + 256 u, the input of this
   //    thread's first radix-16 butterfly: that pass runs in registers.
   fft_fwd_from_regs<12, T>(buf, tw, x, tid);
-  // 3. DFT_N input (bit-reversed source slot, n >= k reads bin n + 1)
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    x[u] = make_double2(0.0, 0.0);
-    if (n < N) {
-      const int src = n < k ? n : n + 1;
-      x[u] = cmul(buf[swz(fft_brev<12>(src))], __ldg(&F.phS[n]));
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    if (n < N) buf[n] = x[u];
-  }
-  __syncthreads();
-  // 4. inverse DFT_N by the prime-factor engine; rings t and N-1-t
-  pfa4095<true>(buf, tid, T);
+  // 3-4. inverse DFT_N by the prime-factor engine, its input (bit-reversed
+  //      source slot, n >= k reads bin n + 1) formed in the gather of the
+  //      first pass; rings t and N-1-t
+  pfa4095_from<true, T>(buf, tid, [&](int n, int g) {
+    const int src = n < k ? n : n + 1;
+    return cmul(buf[swz(fft_brev<12>(src))], __ldg(&F.phS[g]));
+  });
   constexpr int dpos = (int)(((unsigned)T * (unsigned)PFA_STEP) % (unsigned)PFA_N);
   int pos = pfa_pos(tid), posr = pfa_pos(N - 1 - tid);  // slots of rings t and N-1-t
 #pragma unroll 4

@@ -185,6 +185,59 @@ S2W_DEV void pfa_pass(double2* __restrict__ buf, int tid, int nthr) {
   pfa_pass_n<PFA_N, P, INV>(buf, tid, nthr);
 }
 
+// pfa_pass_n whose input comes from src(i, g) (element i of the row to be
+// transformed; g = j * (NN / P) + r its position in gather order, contiguous
+// across the threads) instead of buf[i]: every line of axis P is gathered into
+// registers, then -- after a barrier, so src may read buf itself -- transformed
+// and written to its slots.  Replaces a separate staging pass of the row
+// through shared memory.  Not synced at the end.
+template <int NN, int P, bool INV, int T, class Src>
+S2W_DEV void pfa_pass_gather(double2* __restrict__ buf, int tid, Src src) {
+  constexpr int A = NN / P;              // number of lines
+  constexpr int RR = (A + T - 1) / T;    // lines per thread
+  double2 v[RR][P];
+#pragma unroll
+  for (int rr = 0; rr < RR; ++rr) {
+    const int r = tid + rr * T;
+    if (RR * T != A && r >= A) break;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      int i = P * r + j * A;
+      if (i >= NN) i -= NN;
+      v[rr][j] = src(i, j * A + r);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < RR; ++rr) {
+    const int r = tid + rr * T;
+    if (RR * T != A && r >= A) break;
+    dft_p<P, INV>(v[rr]);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      int i = P * r + j * A;
+      if (i >= NN) i -= NN;
+      buf[i] = v[rr][j];
+    }
+  }
+}
+
+// pfa4095 with the row supplied by src (see pfa_pass_gather): the axis-9 pass
+// comes first (455 lines: two per thread at T = 256, 18 values in registers),
+// the axes commute.  Every thread may still be reading buf through src on
+// entry.  Ends synced.
+template <bool INV, int T, class Src>
+S2W_DEV void pfa4095_from(double2* buf, int tid, Src src) {
+  pfa_pass_gather<PFA_N, 9, INV, T>(buf, tid, src);
+  __syncthreads();
+  pfa_pass<13, INV>(buf, tid, T);
+  __syncthreads();
+  pfa_pass<7, INV>(buf, tid, T);
+  __syncthreads();
+  pfa_pass<5, INV>(buf, tid, T);
+  __syncthreads();
+}
+
 // Slot of output bin k after pfa4095: sum_i (k mod P_i)(N/P_i) mod N, and
 // since P_i (N/P_i) = N that is k * sum_i N/P_i = 2174 k (mod N).  Additive:
 // pfa_pos(k + d) = pfa_pos(k) + pfa_pos(d) (mod N).

@@ -39,7 +39,8 @@ struct FftTablesDev {
   const double* w2s;      // [4096] FFT(w_hat(2d), circular)/4096 (real: the kernel is real and even),
                           //        the |sin| series on one parity class, bit-reversed
   const double2* phA;     // [N]  e^{-i pi q/N} / N  (theta: DFT_N bin -> Fourier coefficient)
-  const double2* phS;     // [N]  e^{-i pi q/N2} e^{i pi q/N} / N2  (theta_syn: DFT_N2 bin -> DFT_N input)
+  const double2* phS;     // [N]  e^{-i pi q/N2} e^{i pi q/N} / N2  (theta_syn: DFT_N2 bin -> DFT_N input);
+                          //      N = 4095: in the gather order of the axis-9 prime-factor pass (capi.cu)
   // N = 8191 (k = 4096) stage kernels ("k4"; phA / phS above, tw = the 8192-point engine):
   const int* rgpow;       // [8190] Rader gather g^q mod N
   const int* rplog;       // [N]    Rader output map bin g^-p -> p

@@ -200,26 +200,16 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   }
   __syncthreads();
   mbar_wait(mb, 0);
-  // 1. parity extension to the full circle (natural order for the PFA)
+  // 1-2. DFT_N of the parity extension to the full circle: the extended
+  //      samples are formed in the gather of the first prime-factor pass
   double2 x[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
+  pfa4095_from<false, T>(buf, tid, [&](int n, int) {
     const bool lo = n < k;
     const int src = lo ? n : 2 * k - 2 - n;
-    const double2 e = (has_e && n < N) ? buf[src] : make_double2(0.0, 0.0);
-    const double2 o = (has_o && n < N) ? buf[k + src] : make_double2(0.0, 0.0);
-    x[u] = lo ? cadd(e, o) : csub(e, o);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    if (n < N) buf[n] = x[u];
-  }
-  __syncthreads();
-  // 2. DFT_N
-  pfa4095<false>(buf, tid, T);
+    const double2 e = has_e ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = has_o ? buf[k + src] : make_double2(0.0, 0.0);
+    return lo ? cadd(e, o) : csub(e, o);
+  });
   // 3-8. coefficient split, parity-class convolutions, evaluation FFT (N2 = 4096)
   static_assert(U == 16, "theta_classes scratch");
   theta_classes<12, T>(buf, side, tw, F, F.w2s, x, [&](int bin) { return buf[pfa_pos(bin)]; });
