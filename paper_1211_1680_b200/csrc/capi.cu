@@ -874,7 +874,12 @@ static int build_grid(GridRes* g, int dev, int scheme, int k) {
     CHECK(upload_new(&g->rD, Dslot));
     CHECK(upload_new(&g->w4s, w4r));
     CHECK(upload_new(&g->phA, phA));
-    CHECK(upload_new(&g->phS, phS));
+    // theta_syn_k4 applies phS in Rader's input gather (rader8191_from: entry q
+    // is sample g^q, entry 8190 sample 0): stored in that order
+    std::vector<double2> phSg(N);
+    for (int q = 0; q < N - 1; ++q) phSg[q] = phS[gpow[q]];
+    phSg[N - 1] = phS[0];
+    CHECK(upload_new(&g->phS, phSg));
   }
   if (scheme == S2W_SCHEME_MW) CHECK(theta_setup(g));
   return S2W_OK;

@@ -1333,25 +1333,14 @@ __global__ void __launch_bounds__(T, 1) theta_syn_k4_kernel(ThetaSynArgs a) {
   __syncthreads();
   // x[u] is element tid + 512 u: the first radix-16 pass runs in registers
   fft_fwd_from_regs<13, T>(buf, tw, x, tid);
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    x[u] = make_double2(0.0, 0.0);
-    if (n < N) {
-      const int src = n < k ? n : n + 1;
-      x[u] = cmul(buf[swz(fft_brev<13>(src))], __ldg(&F.phS[n]));
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    if (n < N) buf[n] = x[u];
-  }
-  __syncthreads();
+  // inverse DFT_N (Rader), its input (bit-reversed source slot, n >= k reads
+  // bin n + 1, times phS) formed in Rader's input gather
   const RaderTabs R = rader_tabs(F);
   double2 x0, X0;
-  rader8191<T, true>(buf, R, part, x0, X0);
+  rader8191_from<T, true>(buf, R, part, x0, X0, [&](int n, int g) {
+    const int src = n < k ? n : n + 1;
+    return cmul(buf[swz(fft_brev<13>(src))], __ldg(&F.phS[g]));
+  });
 #pragma unroll 4
   for (int t = tid; t < k; t += T)
     theta_syn_store(Rw, a, t, rader_bin<true>(buf, R, x0, X0, t), rader_bin<true>(buf, R, x0, X0, N - 1 - t));
@@ -1377,28 +1366,17 @@ __global__ void __launch_bounds__(T, 1) theta_k4_kernel(ThetaArgs a) {
   }
   __syncthreads();
   mbar_wait(mb, 0);
-  // 1. parity extension (natural order)
+  // 1-2. DFT_N (Rader) of the parity extension, formed in Rader's input gather
   double2 x[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    const bool lo = n < k;
-    const int src = lo ? n : 2 * k - 2 - n;
-    const double2 e = (has_e && n < N) ? buf[src] : make_double2(0.0, 0.0);
-    const double2 o = (has_o && n < N) ? buf[k + src] : make_double2(0.0, 0.0);
-    x[u] = lo ? cadd(e, o) : csub(e, o);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n = tid + u * T;
-    if (n < N) buf[n] = x[u];
-  }
-  __syncthreads();
-  // 2. DFT_N (Rader)
   const RaderTabs R = rader_tabs(F);
   double2 x0, X0;
-  rader8191<T, false>(buf, R, part, x0, X0);
+  rader8191_from<T, false>(buf, R, part, x0, X0, [&](int n, int) {
+    const bool lo = n < k;
+    const int src = lo ? n : 2 * k - 2 - n;
+    const double2 e = has_e ? buf[src] : make_double2(0.0, 0.0);
+    const double2 o = has_o ? buf[k + src] : make_double2(0.0, 0.0);
+    return lo ? cadd(e, o) : csub(e, o);
+  });
   // 3-8. coefficient split, parity-class convolutions, evaluation FFT
   //      (N2 = 8192), as theta_k2; rings j and N2-1-j, split by parity
   static_assert(U == 16, "theta_classes scratch");

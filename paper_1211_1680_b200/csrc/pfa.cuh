@@ -299,8 +299,13 @@ struct RaderTabs {
 // written and synced) by T threads.  Leaves the convolution in buf[0, 8190)
 // and returns x_0 and X_0 (of the conjugated input when INV); the outputs are
 // then rader_bin(...).  s_part: T/32 double2 of shared scratch.  Ends synced.
-template <int T, bool INV>
-S2W_DEV void rader8191(double2* buf, const RaderTabs& R, double2* s_part, double2& x0, double2& X0) {
+//
+// rader8191_from: the row comes from src(n, g) (sample n; g = its position in
+// gather order, n = g^q at g = q and n = 0 at g = RADER_M) instead of buf[n];
+// src may read buf (all reads precede the first barrier).
+template <int T, bool INV, class Src>
+S2W_DEV void rader8191_from(double2* buf, const RaderTabs& R, double2* s_part, double2& x0, double2& X0,
+                            Src src) {
   constexpr int U = (RADER_M + T - 1) / T;
   const int tid = threadIdx.x;
   double2 v[U];
@@ -310,12 +315,12 @@ S2W_DEV void rader8191(double2* buf, const RaderTabs& R, double2* s_part, double
     const int q = tid + u * T;
     v[u] = make_double2(0.0, 0.0);
     if (q < RADER_M) {
-      v[u] = buf[__ldg(&R.gpow[q])];
+      v[u] = src(__ldg(&R.gpow[q]), q);
       if (INV) v[u] = cconj(v[u]);
       sum = cadd(sum, v[u]);  // every n >= 1 is some g^q exactly once
     }
   }
-  x0 = buf[0];
+  x0 = src(0, RADER_M);
   if (INV) x0 = cconj(x0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -336,6 +341,11 @@ S2W_DEV void rader8191(double2* buf, const RaderTabs& R, double2* s_part, double
   for (int s = tid; s < RADER_M; s += T) buf[s] = cmul(buf[s], __ldg(&R.D[s]));
   __syncthreads();
   pfa8190<true>(buf, tid, T);
+}
+
+template <int T, bool INV>
+S2W_DEV void rader8191(double2* buf, const RaderTabs& R, double2* s_part, double2& x0, double2& X0) {
+  rader8191_from<T, INV>(buf, R, s_part, x0, X0, [&](int n, int) { return buf[n]; });
 }
 
 // Output bin b of rader8191 (conjugated back when INV).

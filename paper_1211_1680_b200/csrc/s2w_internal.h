@@ -40,7 +40,8 @@ struct FftTablesDev {
                           //        the |sin| series on one parity class, bit-reversed
   const double2* phA;     // [N]  e^{-i pi q/N} / N  (theta: DFT_N bin -> Fourier coefficient)
   const double2* phS;     // [N]  e^{-i pi q/N2} e^{i pi q/N} / N2  (theta_syn: DFT_N2 bin -> DFT_N input);
-                          //      N = 4095: in the gather order of the axis-9 prime-factor pass (capi.cu)
+                          //      N = 4095: in the gather order of the axis-9 prime-factor pass, N = 8191: in
+                          //      Rader's gather order (capi.cu)
   // N = 8191 (k = 4096) stage kernels ("k4"; phA / phS above, tw = the 8192-point engine):
   const int* rgpow;       // [8190] Rader gather g^q mod N
   const int* rplog;       // [N]    Rader output map bin g^-p -> p
