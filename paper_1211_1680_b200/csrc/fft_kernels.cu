@@ -1186,26 +1186,16 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
   }
   __syncthreads();
   mbar_wait(mb, 0);
-  if (a.real) {
-    const double* r = reinterpret_cast<const double*>(buf);
-    double xr[U], xi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n = tid + u * T;
-      xr[u] = n < N ? r[n] : 0.0;
-      xi[u] = (n < N && vb) ? r[N + n] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n = tid + u * T;
-      if (n < N) buf[n] = make_double2(xr[u], xi[u]);
-    }
-    __syncthreads();
-  }
   const RaderTabs R = rader_tabs(a.T);
   double2 x0, X0;
-  rader8191<T, false>(buf, R, part, x0, X0);
+  if (a.real) {
+    // [ring a | ring b] doubles -> z = a + i b, formed in Rader's input gather
+    const double* r = reinterpret_cast<const double*>(buf);
+    rader8191_from<T, false>(buf, R, part, x0, X0,
+                             [&](int n, int) { return make_double2(r[n], vb ? r[N + n] : 0.0); });
+  } else {
+    rader8191<T, false>(buf, R, part, x0, X0);
+  }
 #pragma unroll 4
   for (int mi = tid; mi < a.n_bins; mi += T) {
     const double2 z = rader_bin<false>(buf, R, x0, X0, mi);
@@ -1249,35 +1239,25 @@ __global__ void __launch_bounds__(T, 1) phi_inv_k4_kernel(PhiInvArgs a) {
   }
   __syncthreads();
   mbar_wait(mb, 0);
-  if (a.real) {
-    double2 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n = tid + u * T;
-      x[u] = make_double2(0.0, 0.0);
-      if (n < N) {
-        const bool lo = n < nb;
-        const int src = lo ? n : N - n;
-        double2 X = buf[src], Y = vb ? buf[nb + src] : make_double2(0.0, 0.0);
-        if (!lo) {
-          X = cconj(X);
-          Y = cconj(Y);
-        }
-        if (n == 0) X.y = Y.y = 0.0;
-        x[u] = cadd(X, cmul_pi(Y));
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n = tid + u * T;
-      if (n < N) buf[n] = x[u];
-    }
-    __syncthreads();
-  }
   const RaderTabs R = rader_tabs(a.T);
   double2 x0, X0;
-  rader8191<T, true>(buf, R, part, x0, X0);
+  if (a.real) {
+    // Hermitian spectra of the two rings (irfft ignores Im of the DC bin),
+    // formed in Rader's input gather
+    rader8191_from<T, true>(buf, R, part, x0, X0, [&](int n, int) {
+      const bool lo = n < nb;
+      const int src = lo ? n : N - n;
+      double2 X = buf[src], Y = vb ? buf[nb + src] : make_double2(0.0, 0.0);
+      if (!lo) {
+        X = cconj(X);
+        Y = cconj(Y);
+      }
+      if (n == 0) X.y = Y.y = 0.0;
+      return cadd(X, cmul_pi(Y));
+    });
+  } else {
+    rader8191<T, true>(buf, R, part, x0, X0);
+  }
   const int pole_ring = (N + 1) / 2 - 1 - a.t_offset;
   const bool pa = a.mw_pole && ta == pole_ring, pb = a.mw_pole && vb && ta + 1 == pole_ring;
   const double2 pva = pa ? __ldg(&Ga[0]) : make_double2(0.0, 0.0);
