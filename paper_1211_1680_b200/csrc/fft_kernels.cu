@@ -1183,6 +1183,13 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
     mbar_init(mb, 1);
     mbar_expect_tx(mb, bytes);
     bulk_g2s(buf, a.in + (a.real ? base_a : 2 * base_a), bytes, mb);
+    // the row of the CTA that will take this slot later (as the k2 kernels)
+    const int nrow = row + a.pfd;
+    if (a.pfd && nrow < (int)gridDim.x) {
+      const int ns = nrow / per, np = nrow - ns * per;
+      const long long nb = ((long long)ns * a.n_rings + (a.real ? 2 * np : np)) * N;
+      bulk_prefetch_l2(a.in + (a.real ? nb : 2 * nb), bytes);
+    }
   }
   __syncthreads();
   mbar_wait(mb, 0);
@@ -1236,6 +1243,13 @@ __global__ void __launch_bounds__(T, 1) phi_inv_k4_kernel(PhiInvArgs a) {
     mbar_init(mb, 1);
     mbar_expect_tx(mb, bytes);
     bulk_g2s(buf, Ga, bytes, mb);
+    const int nrow = row + a.pfd;
+    if (a.pfd && nrow < (int)gridDim.x) {
+      const int ns = nrow / per, np = nrow - ns * per;
+      const int nta = a.real ? 2 * np : np;
+      const bool nvb = a.real && nta + 1 < a.n_rings;
+      bulk_prefetch_l2(a.in + ((size_t)ns * a.n_rings + nta) * nb, (nvb ? 2u : 1u) * nb * 16u);
+    }
   }
   __syncthreads();
   mbar_wait(mb, 0);
