@@ -1170,7 +1170,7 @@ __global__ void __launch_bounds__(T, 1) phi_fwd_k4_kernel(PhiFwdArgs a) {
   double2* buf = smem;                 // [8192]
   double2* part = smem + K4_M;         // [T/32]
   uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
-  constexpr int N = K4_N, U = (K4_N + T - 1) / T;
+  constexpr int N = K4_N;
   const int tid = threadIdx.x;
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
   const int row = blockIdx.x;
@@ -1228,7 +1228,7 @@ __global__ void __launch_bounds__(T, 1) phi_inv_k4_kernel(PhiInvArgs a) {
   double2* buf = smem;
   double2* part = smem + K4_M;
   uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
-  constexpr int N = K4_N, U = (K4_N + T - 1) / T;
+  constexpr int N = K4_N;
   const int tid = threadIdx.x;
   const int per = a.real ? (a.n_rings + 1) / 2 : a.n_rings;
   const int row = blockIdx.x;
@@ -1348,7 +1348,7 @@ __global__ void __launch_bounds__(T, 1) theta_k4_kernel(ThetaArgs a) {
   double2* tw = side + K4_K;         // [546]
   double2* part = tw + K4_NTW;       // [T/32]
   uint64_t* mb = reinterpret_cast<uint64_t*>(part + T / 32);
-  constexpr int N = K4_N, k = K4_K, U = K4_M / T;
+  constexpr int k = K4_K, U = K4_M / T;
   const FftTablesDev& F = a.T;
   const int tid = threadIdx.x;
   bool has_e, has_o;

@@ -180,7 +180,7 @@ S2W_DEV void theta_k2_row(const ThetaArgs& a, int row, double2* smem, int pf) {
   double2* side = smem + K2_M;       // [2048]
   double2* tw = side + K2_K;         // [272]
   uint64_t* mb = reinterpret_cast<uint64_t*>(tw + K2_NTW);
-  constexpr int N = K2_N, k = K2_K, U = K2_M / T, V = K2_K / T;
+  constexpr int k = K2_K, U = K2_M / T;
   const FftTablesDev& F = a.T;
   const int tid = threadIdx.x;
   bool has_e, has_o;
