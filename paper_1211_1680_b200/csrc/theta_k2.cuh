@@ -101,7 +101,7 @@ S2W_DEV void k2_issue(uint64_t* mb, double2* tw, const double2* gtw, double2* ds
 //  * 7 -> 8: X'_n = conj(H'(q)) e^{-i pi q/M}, n = q mod M, is gathered as
 //    element tid + T u: the input of the first butterfly of the FFT.
 // x: 16 registers of scratch.  Precondition: bin_value's source written and
-// synced.
+// synced, side unused.
 template <int LOGM, int T, class Bin>
 S2W_DEV void theta_classes(double2* buf, double2* side, const double2* tw, const FftTablesDev& F,
                            const double* __restrict__ wtab, double2* x, Bin bin_value) {
@@ -110,7 +110,7 @@ S2W_DEV void theta_classes(double2* buf, double2* side, const double2* tw, const
   const int tid = threadIdx.x;
   const int sb = swz(tid);
   {
-    double2 vo[8];
+    // (side is free until here: the odd class goes there at once)
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
       if (kk >= 4 && kk < 12) {
@@ -121,12 +121,9 @@ S2W_DEV void theta_classes(double2* buf, double2* side, const double2* tw, const
       const int be = 2 * aa + (aa < 0 ? N : 0);        // bin of q = 2 aa
       const int bo = be + 1;                           // bin of q = 2 aa + 1
       x[kk] = aa > -(M / 4) ? cmul(bin_value(be), __ldg(&F.phA[be])) : make_double2(0.0, 0.0);
-      vo[kk & 7] = cmul(bin_value(bo), __ldg(&F.phA[bo]));
+      side[(tid + T * kk) & (k - 1)] = cmul(bin_value(bo), __ldg(&F.phA[bo]));
     }
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk)
-      if (kk < 4 || kk >= 12) side[(tid + T * kk) & (k - 1)] = vo[kk & 7];
     bfly16<false>(x, tw[tid]);
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) buf[sb ^ swz(kk * T)] = x[kk];
