@@ -10,7 +10,8 @@ int io_fail(int code, const char* fmt, ...);
 
 // ------------------------------------------------------------------ FFT tables
 // Per grid band k (N = 2k-1, M = 2^logM >= 2N-1).  All spectra are stored in
-// bit-reversed order (see fft.cuh) and carry the 1/M of the unnormalised
+// bit-reversed order, transposed for the engine's core pass (fft.cuh
+// conv_core; capi.cu core_transpose), and carry the 1/M of the unnormalised
 // inverse FFT.
 constexpr int FFT_MAX_LOGM_SMEM = 13;  // one 128 KiB row per CTA; larger M uses split mode
 
