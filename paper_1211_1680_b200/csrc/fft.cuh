@@ -232,17 +232,33 @@ S2W_DEV void conv_core_real(double2* __restrict__ buf, const double* __restrict_
   }
 }
 
+// Barrier between the innermost radix-16 pass (span 2^CB) and the core pass
+// (radix 2^CB at span 1).  When CB = 4 (LOGM = 8, 12) and every thread has one
+// butterfly per pass, both passes of a 256-element block belong to the same 16
+// threads (pass: block b >> 4, position b & 15; core: elements 16 b ..), i.e.
+// to one half-warp: a warp-level barrier orders them and the warps run pass,
+// core and inverse pass without waiting for one another.
+template <int LOGM, int GS>
+S2W_DEV void sync_core() {
+  if constexpr (LOGM - 4 * fft_k16(LOGM) == 4 && GS * 16 == (1 << LOGM) && GS >= 32) __syncwarp();
+  else __syncthreads();
+}
+
 // tw: table of the size 2^(LOGM + TWSH) (TWSH = 0 or 1), i.e. for a
 // half-size transform the engine's own table read at stride 2.
+// Ends synced for the core pass (sync_core), i.e. for the whole CTA unless
+// sync_core is the warp-level barrier.
 template <int LOGM, int GS, int P, int TWSH = 0>
 S2W_DEV void fwd_passes(double2* buf, const double2* tw, int gtid) {
   if constexpr (P < fft_k16(LOGM)) {
     pass16<LOGM, GS, LOGM - 4 * (P + 1), false, 1 << TWSH>(
         buf, tw + fft_tw_off(LOGM + TWSH, P), gtid);
-    __syncthreads();
+    if constexpr (P == fft_k16(LOGM) - 1) sync_core<LOGM, GS>();
+    else __syncthreads();
     fwd_passes<LOGM, GS, P + 1, TWSH>(buf, tw, gtid);
   }
 }
+// Precondition: the core pass's writes ordered by sync_core (P = last pass).
 template <int LOGM, int GS, int P, int PMIN = 0>
 S2W_DEV void inv_passes(double2* buf, const double2* tw, int gtid) {
   if constexpr (P >= PMIN) {
@@ -293,7 +309,7 @@ S2W_DEV void fft_conv(double2* buf, const double2* tw, const double2* __restrict
                       int gtid) {
   fwd_passes<LOGM, GS, 0>(buf, tw, gtid);
   conv_core<LOGM, GS>(buf, tab, gtid);
-  __syncthreads();
+  sync_core<LOGM, GS>();
   inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
 }
 
@@ -302,7 +318,7 @@ template <int LOGM, int GS>
 S2W_DEV void fft_conv_real(double2* buf, const double2* tw, const double* __restrict__ tab, int gtid) {
   fwd_passes<LOGM, GS, 0>(buf, tw, gtid);
   conv_core_real<LOGM, GS>(buf, tab, gtid);
-  __syncthreads();
+  sync_core<LOGM, GS>();
   inv_passes<LOGM, GS, fft_k16(LOGM) - 1>(buf, tw, gtid);
 }
 
@@ -315,7 +331,7 @@ S2W_DEV void fft_conv_real_inner(double2* buf, const double2* tw, const double* 
                                  int gtid) {
   fwd_passes<LOGM, GS, 1>(buf, tw, gtid);
   conv_core_real<LOGM, GS>(buf, tab, gtid);
-  __syncthreads();
+  sync_core<LOGM, GS>();
   inv_passes<LOGM, GS, fft_k16(LOGM) - 1, 1>(buf, tw, gtid);
 }
 
