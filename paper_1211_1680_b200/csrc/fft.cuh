@@ -244,6 +244,15 @@ S2W_DEV void sync_core() {
   else __syncthreads();
 }
 
+// Barrier between the radix-16 passes at spans 2^LS and 2^(LS-4): the 2^(LS+4)
+// elements of a block of the wider pass belong to the same 2^LS consecutive
+// threads in both (one butterfly per thread), so at LS <= 5 that is one warp.
+template <int LOGM, int GS, int LS>
+S2W_DEV void sync_pass() {
+  if constexpr (LS <= 5 && GS * 16 == (1 << LOGM) && GS >= 32) __syncwarp();
+  else __syncthreads();
+}
+
 // tw: table of the size 2^(LOGM + TWSH) (TWSH = 0 or 1), i.e. for a
 // half-size transform the engine's own table read at stride 2.
 // Ends synced for the core pass (sync_core), i.e. for the whole CTA unless
@@ -254,7 +263,7 @@ S2W_DEV void fwd_passes(double2* buf, const double2* tw, int gtid) {
     pass16<LOGM, GS, LOGM - 4 * (P + 1), false, 1 << TWSH>(
         buf, tw + fft_tw_off(LOGM + TWSH, P), gtid);
     if constexpr (P == fft_k16(LOGM) - 1) sync_core<LOGM, GS>();
-    else __syncthreads();
+    else sync_pass<LOGM, GS, LOGM - 4 * (P + 1)>();
     fwd_passes<LOGM, GS, P + 1, TWSH>(buf, tw, gtid);
   }
 }
@@ -263,7 +272,8 @@ template <int LOGM, int GS, int P, int PMIN = 0>
 S2W_DEV void inv_passes(double2* buf, const double2* tw, int gtid) {
   if constexpr (P >= PMIN) {
     pass16<LOGM, GS, LOGM - 4 * (P + 1), true>(buf, tw + fft_tw_off(LOGM, P), gtid);
-    __syncthreads();
+    if constexpr (P > PMIN) sync_pass<LOGM, GS, LOGM - 4 * P>();  // next: span 2^(LS + 4)
+    else __syncthreads();
     inv_passes<LOGM, GS, P - 1, PMIN>(buf, tw, gtid);
   }
 }
